@@ -1,0 +1,27 @@
+"""B200-native TP-EP hybrid MoE layer (MixServe, arxiv 2601.08800).
+
+Drop-in for the hot path of the reference ``moeplan`` toolkit: the fused
+AG-dispatch / expert / RS-combine MoE layer forward and its routing table,
+plus the reference-compatible trace.  The data path runs in hand-written
+sm_100a CUDA kernels behind the C-ABI in ``include/mixserve_b200.h``.
+"""
+
+__version__ = "0.1.0"
+
+from .errors import (AnalyzerError, CalibrationError, CapacityError,  # noqa: F401
+                     ConfigError, GrammarError, MoeplanError, SaturationError,
+                     SchedulingError, StrategyError, VerificationError)
+from .simcluster import (ExpertSpec, RouterSpec, SimCluster, SwiGLUExperts,  # noqa: F401
+                         TraceEvent, build_cluster, build_routing_table,
+                         fused_ag_dispatch, fused_rs_combine, moe_oracle,
+                         run_moe_block, verify_against_oracle)
+
+__all__ = [
+    "__version__",
+    "AnalyzerError", "CalibrationError", "CapacityError", "ConfigError",
+    "ExpertSpec", "GrammarError", "MoeplanError", "RouterSpec",
+    "SaturationError", "SchedulingError", "SimCluster", "StrategyError",
+    "SwiGLUExperts", "TraceEvent", "VerificationError", "build_cluster",
+    "build_routing_table", "fused_ag_dispatch", "fused_rs_combine",
+    "moe_oracle", "run_moe_block", "verify_against_oracle",
+]

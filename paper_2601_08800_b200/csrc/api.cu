@@ -1,0 +1,547 @@
+// api.cu -- the extern "C" boundary (include/mixserve_b200.h): symmetric
+// heap communicator, layer plan, phase sequencing and the device barrier.
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mx_internal.cuh"
+
+namespace mx {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  set_error("CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+            file, line, what);
+  return MX_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- barrier
+// All ranks: publish the epoch into every peer's flag slot (release, system
+// scope), then wait until every peer has published it into ours (acquire).
+// One thread per peer.  A watchdog turns a lost peer into an error flag
+// instead of a hang (SURVEY.md §5 failure detection).
+__global__ void k_barrier(DevView v, unsigned long long epoch) {
+  const int r = threadIdx.x;
+  if (r < v.W) {
+    __threadfence_system();
+    st_release_sys(at<unsigned long long>(v, r, v.off.flags) + v.rank, epoch);
+    const unsigned long long* mine = at<unsigned long long>(v, v.rank, v.off.flags) + r;
+    long long t0 = clock64();
+    while (ld_acquire_sys(mine) < epoch) {
+      if (clock64() - t0 > (long long)20000000000LL) {  // ~10 s at 2 GHz
+        atomicOr(at<int>(v, v.rank, v.off.err) + 2, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+int launch_barrier(const DevView& v, unsigned long long epoch, cudaStream_t s) {
+  k_barrier<<<1, 64, 0, s>>>(v, epoch);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static int elt_bytes(int dt) { return dt == MX_F64 ? 8 : dt == MX_F32 ? 4 : 2; }
+
+static long long default_capacity(const mx_plan_desc& d) {
+  // worst case: every token of every group lands on one host with
+  // min(k, experts on that host) slots each
+  const int per_host = (d.num_experts + d.n_group - 1) / d.n_group;
+  const int kk = d.top_k < per_host ? d.top_k : per_host;
+  return (long long)d.tokens * d.n_group * kk;
+}
+
+static int validate(const mx_plan_desc& d) {
+  if (d.n_group < 1 || d.tp < 1) { set_error("cluster needs at least one node and one device"); return MX_ERR_INVALID; }
+  if (d.n_group * d.tp > MX_MAXW) { set_error("world size %d exceeds %d", d.n_group * d.tp, MX_MAXW); return MX_ERR_UNSUPPORTED; }
+  if (d.n_group > MX_NMAX) { set_error("n_group %d exceeds %d", d.n_group, MX_NMAX); return MX_ERR_UNSUPPORTED; }
+  if (d.tokens < 0 || d.hidden < 1) { set_error("bad tokens/hidden"); return MX_ERR_INVALID; }
+  if (d.num_experts < 1 || d.num_experts > MX_EMAX) { set_error("num_experts %d outside [1, %d]", d.num_experts, MX_EMAX); return MX_ERR_UNSUPPORTED; }
+  if (d.top_k < 1 || d.top_k > d.num_experts) { set_error("top_k must be in [1, num_experts]"); return MX_ERR_INVALID; }
+  if (d.top_k > MX_KMAX) { set_error("top_k %d exceeds %d", d.top_k, MX_KMAX); return MX_ERR_UNSUPPORTED; }
+  if (d.act_dtype < MX_F64 || d.act_dtype > MX_BF16) { set_error("bad act_dtype"); return MX_ERR_INVALID; }
+  if (d.expert_kind == MX_EXPERT_SWIGLU) {
+    if (d.act_dtype != MX_BF16) { set_error("SwiGLU experts run in bf16"); return MX_ERR_UNSUPPORTED; }
+    if (d.inter % d.tp != 0 || (d.inter / d.tp) % 128 != 0) { set_error("inter/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED; }
+    if (d.hidden % 128 != 0) { set_error("hidden must be a multiple of 128 for the grouped GEMM"); return MX_ERR_UNSUPPORTED; }
+  } else if (d.expert_kind != MX_EXPERT_AFFINE) {
+    set_error("bad expert_kind"); return MX_ERR_INVALID;
+  }
+  return MX_OK;
+}
+
+static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
+  Offsets o{};
+  size_t p = 0;
+  auto take = [&](size_t bytes) { size_t at = p; p = align_up(p + bytes, 1024); return at; };
+  const size_t T = d.tokens, k = d.top_k, E = d.num_experts, n = d.n_group, h = d.hidden;
+  const size_t C = (T + MX_CHUNK - 1) / MX_CHUNK;
+  const size_t elt = elt_bytes(d.act_dtype);
+  const size_t wsz = d.act_dtype == MX_F64 ? 8 : 4;
+  const size_t It = d.expert_kind == MX_EXPERT_SWIGLU ? d.inter / d.tp : 0;
+  o.flags = take(8 * MX_MAXW);
+  o.cnt_all = take(4 * n * E);
+  o.counters = take(4 * 16);
+  o.err = take(4 * 16);
+  o.recv = take((size_t)cap * h * elt);
+  o.partial = take((size_t)cap * h * elt);
+  o.y = take(T * h * elt);
+  o.act = take((size_t)cap * It * 2);
+  o.ids = take(4 * T * k);
+  o.w = take(wsz * T * k);
+  o.slot_pos = take(4 * T * k);
+  o.slot_tm = take(4 * T * k);
+  o.slot_rank = take(4 * T * k);
+  o.slot_tmr = take(4 * T * k);
+  o.chunk_hist = take(4 * C * E);
+  o.chunk_host = take(4 * C * n);
+  o.exp_off = take(4 * E);
+  o.exp_cnt = take(4 * E);
+  o.grp_off = take(4 * n * E);
+  o.send = take(4 * n * n);
+  o.tm_off = take(4 * n * n);
+  o.host_rows = take(4 * n);
+  o.total = p;
+  return o;
+}
+
+}  // namespace mx
+
+using namespace mx;
+
+struct mx_comm {
+  int n = 0, m = 0, W = 0, rank = 0, emulate = 0, device = 0;
+  size_t heap_bytes = 0;
+  char* heap[MX_MAXW] = {};
+  bool owned[MX_MAXW] = {};
+  unsigned long long epoch = 0;
+  Offsets off{};       // of the plan using this heap (flags live at 0)
+  bool has_plan = false;
+};
+
+struct mx_plan {
+  mx_comm* comm = nullptr;
+  mx_plan_desc d{};
+  long long cap = 0;
+  Offsets off{};
+  DevView base{};
+};
+
+static DevView view_for(const mx_plan* p, int r) {
+  DevView v = p->base;
+  v.rank = r;
+  v.group = r / p->d.tp;
+  v.tp_rank = r % p->d.tp;
+  return v;
+}
+
+extern "C" {
+
+int mx_abi_version(void) { return MX_ABI_VERSION; }
+const char* mx_last_error(void) { return g_err.c_str(); }
+
+int mx_device_sm_count(int device, int* out) {
+  MX_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device));
+  return MX_OK;
+}
+
+int mx_comm_create(int n_group, int tp, int rank, int emulate, size_t heap_bytes,
+                   mx_comm** out) {
+  if (n_group < 1 || tp < 1) { set_error("cluster needs at least one node and one device"); return MX_ERR_INVALID; }
+  const int W = n_group * tp;
+  if (W > MX_MAXW) { set_error("world size %d exceeds %d", W, MX_MAXW); return MX_ERR_UNSUPPORTED; }
+  if (!emulate && (rank < 0 || rank >= W)) { set_error("rank %d outside world %d", rank, W); return MX_ERR_INVALID; }
+  mx_comm* c = new mx_comm();
+  c->n = n_group; c->m = tp; c->W = W; c->rank = emulate ? -1 : rank; c->emulate = emulate;
+  c->heap_bytes = align_up(heap_bytes < 4096 ? 4096 : heap_bytes, 2 << 20);
+  cudaGetDevice(&c->device);
+  const int first = emulate ? 0 : rank, last = emulate ? W : rank + 1;
+  for (int r = first; r < last; ++r) {
+    void* ptr = nullptr;
+    cudaError_t e = cudaMalloc(&ptr, c->heap_bytes);
+    if (e != cudaSuccess) {
+      for (int q = first; q < r; ++q) cudaFree(c->heap[q]);
+      delete c;
+      return cuda_fail(e, "cudaMalloc(heap)", __FILE__, __LINE__);
+    }
+    cudaMemset(ptr, 0, c->heap_bytes);
+    c->heap[r] = static_cast<char*>(ptr);
+    c->owned[r] = true;
+  }
+  MX_CUDA(cudaDeviceSynchronize());
+  *out = c;
+  return MX_OK;
+}
+
+int mx_comm_ipc_handle(mx_comm* c, void* handle64) {
+  if (c->emulate) { set_error("emulated communicator has no IPC handle"); return MX_ERR_INVALID; }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  cudaIpcMemHandle_t hd;
+  MX_CUDA(cudaIpcGetMemHandle(&hd, c->heap[c->rank]));
+  memcpy(handle64, &hd, 64);
+  return MX_OK;
+}
+
+int mx_comm_open_peers(mx_comm* c, const void* handles) {
+  if (c->emulate) return MX_OK;
+  const char* hs = static_cast<const char*>(handles);
+  for (int r = 0; r < c->W; ++r) {
+    if (r == c->rank || c->heap[r]) continue;
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, hs + 64 * r, 64);
+    void* ptr = nullptr;
+    MX_CUDA(cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    c->heap[r] = static_cast<char*>(ptr);
+    c->owned[r] = false;
+  }
+  return MX_OK;
+}
+
+int mx_comm_heap(mx_comm* c, int rank, void** base, size_t* bytes) {
+  if (rank < 0 || rank >= c->W) { set_error("bad rank"); return MX_ERR_INVALID; }
+  *base = c->heap[rank];
+  *bytes = c->heap_bytes;
+  return MX_OK;
+}
+
+int mx_comm_destroy(mx_comm* c) {
+  if (!c) return MX_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->W; ++r) {
+    if (!c->heap[r]) continue;
+    if (c->owned[r]) cudaFree(c->heap[r]);
+    else cudaIpcCloseMemHandle(c->heap[r]);
+  }
+  delete c;
+  return MX_OK;
+}
+
+int mx_plan_heap_bytes(const mx_plan_desc* d, size_t* out) {
+  int rc = validate(*d);
+  if (rc) return rc;
+  const long long cap = d->capacity > 0 ? d->capacity : default_capacity(*d);
+  *out = compute_offsets(*d, cap).total;
+  return MX_OK;
+}
+
+int mx_plan_create(mx_comm* c, const mx_plan_desc* d, mx_plan** out) {
+  int rc = validate(*d);
+  if (rc) return rc;
+  if (d->n_group != c->n || d->tp != c->m) {
+    set_error("plan cluster %dx%d mismatches communicator %dx%d", d->n_group, d->tp, c->n, c->m);
+    return MX_ERR_INVALID;
+  }
+  mx_plan* p = new mx_plan();
+  p->comm = c;
+  p->d = *d;
+  p->cap = d->capacity > 0 ? d->capacity : default_capacity(*d);
+  p->off = compute_offsets(*d, p->cap);
+  if (p->off.total > c->heap_bytes) {
+    set_error("plan needs %zu heap bytes, communicator has %zu", p->off.total, c->heap_bytes);
+    delete p;
+    return MX_ERR_INVALID;
+  }
+  DevView& v = p->base;
+  v.n = d->n_group; v.m = d->tp; v.W = c->W;
+  v.T = d->tokens; v.h = d->hidden; v.E = d->num_experts; v.k = d->top_k;
+  v.I_t = d->expert_kind == MX_EXPERT_SWIGLU ? d->inter / d->tp : 0;
+  v.C = (d->tokens + MX_CHUNK - 1) / MX_CHUNK;
+  v.elt = elt_bytes(d->act_dtype);
+  v.renorm = d->renormalize;
+  v.cap = p->cap;
+  v.off = p->off;
+  for (int r = 0; r < c->W; ++r) v.heap[r] = c->heap[r];
+  c->off = p->off;
+  c->has_plan = true;
+  *out = p;
+  return MX_OK;
+}
+
+int mx_plan_destroy(mx_plan* p) {
+  delete p;
+  return MX_OK;
+}
+
+int mx_plan_buffer(mx_plan* p, int rank, int which, void** ptr, size_t* bytes) {
+  const mx_plan_desc& d = p->d;
+  if (rank < 0 || rank >= p->comm->W || !p->comm->heap[rank]) { set_error("bad rank %d", rank); return MX_ERR_INVALID; }
+  const Offsets& o = p->off;
+  const size_t T = d.tokens, k = d.top_k, E = d.num_experts, n = d.n_group, h = d.hidden;
+  const size_t elt = elt_bytes(d.act_dtype);
+  size_t off = 0, len = 0;
+  switch (which) {
+    case MX_BUF_RECV: off = o.recv; len = p->cap * h * elt; break;
+    case MX_BUF_PARTIAL: off = o.partial; len = p->cap * h * elt; break;
+    case MX_BUF_Y: off = o.y; len = T * h * elt; break;
+    case MX_BUF_IDS: off = o.ids; len = 4 * T * k; break;
+    case MX_BUF_WEIGHTS: off = o.w; len = (d.act_dtype == MX_F64 ? 8 : 4) * T * k; break;
+    case MX_BUF_SLOT_POS: off = o.slot_pos; len = 4 * T * k; break;
+    case MX_BUF_SLOT_TM: off = o.slot_tm; len = 4 * T * k; break;
+    case MX_BUF_CNT_ALL: off = o.cnt_all; len = 4 * n * E; break;
+    case MX_BUF_EXP_OFF: off = o.exp_off; len = 4 * E; break;
+    case MX_BUF_EXP_CNT: off = o.exp_cnt; len = 4 * E; break;
+    case MX_BUF_SEND: off = o.send; len = 4 * n * n; break;
+    case MX_BUF_ACT: off = o.act; len = p->cap * (size_t)p->base.I_t * 2; break;
+    default: set_error("bad buffer id %d", which); return MX_ERR_INVALID;
+  }
+  *ptr = p->comm->heap[rank] + off;
+  *bytes = len;
+  return MX_OK;
+}
+
+int mx_comm_barrier(mx_comm* c, void* stream) {
+  if (c->emulate || c->W == 1) return MX_OK;
+  if (!c->has_plan) { set_error("barrier needs a plan on the heap"); return MX_ERR_INVALID; }
+  DevView v{};
+  v.rank = c->rank; v.W = c->W; v.off = c->off;
+  for (int r = 0; r < c->W; ++r) v.heap[r] = c->heap[r];
+  return launch_barrier(v, ++c->epoch, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ phases
+namespace {
+
+struct RankIter {
+  int first, last;
+};
+
+int ranks_for(const mx_plan* p, int rank, RankIter* it) {
+  const mx_comm* c = p->comm;
+  if (c->emulate) {
+    if (rank < 0) { it->first = 0; it->last = c->W; return MX_OK; }
+    if (rank >= c->W) { set_error("rank %d outside world %d", rank, c->W); return MX_ERR_INVALID; }
+    it->first = rank; it->last = rank + 1; return MX_OK;
+  }
+  if (rank >= 0 && rank != c->rank) { set_error("SPMD process of rank %d asked for rank %d", c->rank, rank); return MX_ERR_INVALID; }
+  it->first = c->rank; it->last = c->rank + 1;
+  return MX_OK;
+}
+
+// In emulated mode per-group inputs are stacked [n*T, ...].
+const char* group_ptr(const mx_plan* p, const void* base, int group, size_t per_token_bytes) {
+  if (!base) return nullptr;
+  if (!p->comm->emulate) return static_cast<const char*>(base);
+  return static_cast<const char*>(base) + (size_t)group * p->d.tokens * per_token_bytes;
+}
+
+int barrier(mx_plan* p, cudaStream_t s) {
+  mx_comm* c = p->comm;
+  if (c->emulate || c->W == 1) return MX_OK;
+  DevView v = view_for(p, c->rank);
+  return launch_barrier(v, ++c->epoch, s);
+}
+
+int check_errors(mx_plan* p, int first, int last) {
+  for (int r = first; r < last; ++r) {
+    int err[4];
+    MX_CUDA(cudaMemcpy(err, p->comm->heap[r] + p->off.err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err[1]) { set_error("expert id out of range"); return MX_ERR_INVALID; }
+    if (err[0]) {
+      // report the first host over capacity with its slot count
+      int rows[MX_NMAX];
+      MX_CUDA(cudaMemcpy(rows, p->comm->heap[r] + p->off.host_rows, 4 * p->d.n_group, cudaMemcpyDeviceToHost));
+      for (int d = 0; d < p->d.n_group; ++d)
+        if (rows[d] > p->cap) {
+          set_error("node %d receives %d routed slots, capacity %lld", d, rows[d], p->cap);
+          int zero[4] = {0, 0, 0, 0};
+          cudaMemcpy(p->comm->heap[r] + p->off.err, zero, sizeof(zero), cudaMemcpyHostToDevice);
+          return MX_ERR_CAPACITY;
+        }
+    }
+    if (err[2]) { set_error("peer barrier watchdog expired"); return MX_ERR_TIMEOUT; }
+  }
+  return MX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mx_route(mx_plan* p, int rank, const float* logits, const int32_t* ids, const void* weights,
+             void* stream) {
+  if ((logits == nullptr) == (ids == nullptr)) { set_error("pass exactly one of logits or ids"); return MX_ERR_INVALID; }
+  if (ids && !weights) { set_error("ids need weights"); return MX_ERR_INVALID; }
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t wsz = p->d.act_dtype == MX_F64 ? 8 : 4;
+  for (int r = it.first; r < it.last; ++r) {
+    DevView v = view_for(p, r);
+    rc = launch_route(v, reinterpret_cast<const float*>(group_ptr(p, logits, v.group, 4 * (size_t)p->d.num_experts)),
+                      reinterpret_cast<const int32_t*>(group_ptr(p, ids, v.group, 4 * (size_t)p->d.top_k)),
+                      group_ptr(p, weights, v.group, wsz * p->d.top_k), s);
+    if (rc) return rc;
+  }
+  return MX_OK;
+}
+
+int mx_layout(mx_plan* p, int rank, int check_capacity, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int r = it.first; r < it.last; ++r) {
+    rc = launch_layout(view_for(p, r), s);
+    if (rc) return rc;
+  }
+  if (check_capacity) {
+    MX_CUDA(cudaStreamSynchronize(s));
+    return check_errors(p, it.first, it.last);
+  }
+  return MX_OK;
+}
+
+int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t row = (size_t)p->d.hidden * elt_bytes(p->d.act_dtype);
+  for (int r = it.first; r < it.last; ++r) {
+    DevView v = view_for(p, r);
+    rc = launch_dispatch(v, group_ptr(p, x, v.group, row), s);
+    if (rc) return rc;
+  }
+  return MX_OK;
+}
+
+int mx_expert(mx_plan* p, int rank, const mx_expert_params* ep, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int r = it.first; r < it.last; ++r) {
+    DevView v = view_for(p, r);
+    if (p->d.expert_kind == MX_EXPERT_AFFINE) {
+      rc = launch_expert_affine(v, ep->scales, ep->biases, s);
+    } else {
+      // emulated: per-rank weight shards stacked rank-major
+      const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
+      const int Elmax = (v.E + v.n - 1) / v.n;
+      (void)El;
+      const size_t w13_rank = (size_t)Elmax * 2 * v.I_t * v.h * 2;
+      const size_t w2_rank = (size_t)Elmax * v.h * v.I_t * 2;
+      const int slot = p->comm->emulate ? r : 0;
+      rc = launch_expert_swiglu(v, static_cast<const char*>(ep->w13) + slot * w13_rank,
+                                static_cast<const char*>(ep->w2) + slot * w2_rank, s);
+    }
+    if (rc) return rc;
+  }
+  return MX_OK;
+}
+
+int mx_combine(mx_plan* p, int rank, void* y_out, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int r = it.first; r < it.last; ++r) {
+    rc = launch_combine(view_for(p, r), s);
+    if (rc) return rc;
+  }
+  if (y_out) {
+    rc = barrier(p, s);  // y is complete only after every TP peer pushed
+    if (rc) return rc;
+    const size_t bytes = (size_t)p->d.tokens * p->d.hidden * elt_bytes(p->d.act_dtype);
+    for (int r = it.first; r < it.last; ++r) {
+      const int g = r / p->d.tp;
+      if (p->comm->emulate && (r % p->d.tp) != 0) continue;
+      char* dst = static_cast<char*>(y_out) + (p->comm->emulate ? (size_t)g * bytes : 0);
+      MX_CUDA(cudaMemcpyAsync(dst, p->comm->heap[r] + p->off.y, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return MX_OK;
+}
+
+int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const int32_t* ids,
+               const void* weights, const mx_expert_params* ep, void* y_out, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc;
+  if ((rc = mx_route(p, rank, logits, ids, weights, stream))) return rc;
+  if ((rc = barrier(p, s))) return rc;            // every group's counts published
+  if ((rc = mx_layout(p, rank, 0, stream))) return rc;
+  if ((rc = mx_dispatch(p, rank, x, stream))) return rc;
+  if ((rc = barrier(p, s))) return rc;            // every row landed
+  if ((rc = mx_expert(p, rank, ep, stream))) return rc;
+  if ((rc = barrier(p, s))) return rc;            // every partial written
+  if ((rc = mx_combine(p, rank, nullptr, stream))) return rc;
+  if ((rc = barrier(p, s))) return rc;            // y complete; buffers reusable
+  if (y_out) {
+    RankIter it;
+    if ((rc = ranks_for(p, rank, &it))) return rc;
+    const size_t bytes = (size_t)p->d.tokens * p->d.hidden * elt_bytes(p->d.act_dtype);
+    for (int r = it.first; r < it.last; ++r) {
+      if (p->comm->emulate && (r % p->d.tp) != 0) continue;
+      char* dst = static_cast<char*>(y_out) + (p->comm->emulate ? (size_t)(r / p->d.tp) * bytes : 0);
+      MX_CUDA(cudaMemcpyAsync(dst, p->comm->heap[r] + p->off.y, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return MX_OK;
+}
+
+int mx_baseline_dispatch_pack(mx_plan* p, int rank, const void* x, void* send,
+                              int32_t* counts_out, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  if (it.last - it.first != 1) { set_error("baseline helpers take one rank"); return MX_ERR_INVALID; }
+  DevView v = view_for(p, it.first);
+  const size_t row = (size_t)p->d.hidden * elt_bytes(p->d.act_dtype);
+  return launch_baseline_dispatch_pack(v, group_ptr(p, x, v.group, row), send, counts_out,
+                                       static_cast<cudaStream_t>(stream));
+}
+
+int mx_baseline_dispatch_unpack(mx_plan* p, int rank, const void* recv, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  if (it.last - it.first != 1) { set_error("baseline helpers take one rank"); return MX_ERR_INVALID; }
+  return launch_baseline_dispatch_unpack(view_for(p, it.first), recv, static_cast<cudaStream_t>(stream));
+}
+
+int mx_baseline_combine_pack(mx_plan* p, int rank, void* send, int32_t* counts_out, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  if (it.last - it.first != 1) { set_error("baseline helpers take one rank"); return MX_ERR_INVALID; }
+  return launch_baseline_combine_pack(view_for(p, it.first), send, counts_out,
+                                      static_cast<cudaStream_t>(stream));
+}
+
+int mx_baseline_combine_unpack(mx_plan* p, int rank, const void* recv, void* y, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  if (it.last - it.first != 1) { set_error("baseline helpers take one rank"); return MX_ERR_INVALID; }
+  return launch_baseline_combine_unpack(view_for(p, it.first), recv, y,
+                                        static_cast<cudaStream_t>(stream));
+}
+
+int mx_grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,
+                    const int32_t* cnts, int G, long long M_total, int N, int K, int swiglu,
+                    void* stream) {
+  return grouped_gemm(A, B, D, out_dtype, offs, cnts, nullptr, G, M_total, M_total, N, K, swiglu,
+                      static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// combine.cu -- K4: fused RS-combine (Alg. 1; sim:410-521).
+//
+// Reference schedule per destination: the host group reduce-scatters its TP
+// partials (sim:436-441, sim:455-457), ships each reduced shard back to the
+// token owner (sim:458-475), the owner accumulates w*row (sim:476-483,
+// sim:508-520) and finally all-gathers its shards (sim:500-504).
+//
+// B200 form: owner rank (j,t) PULLS column shard t of every slot's partial
+// from the m TP ranks of the slot's host over NVLink and sums them
+// rank-ascending -- that is the reduce-scatter and the pairwise return in
+// one hop, with the same bytes on the wire -- weights and accumulates in the
+// reference's order (hosts j-1, j-2, ..., j; rows ascending, i.e. experts
+// ascending within a token), then PUSHES the finished shard to every TP rank
+// of its group (the final all-gather).  f64 is uncontracted and therefore
+// bit-identical to the reference.
+#include "mx_internal.cuh"
+
+namespace mx {
+
+template <int DT, bool VEC>
+__global__ void __launch_bounds__(256) k_combine(DevView v) {
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  constexpr int V = VEC ? Elt<DT>::V : 1;  // elements per 16 B vector
+  __shared__ int s_pos[8][MX_KMAX];
+  __shared__ int s_src[8][MX_KMAX];  // first rank of the slot's host group
+  __shared__ A s_w[8][MX_KMAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = v.n, m = v.m, k = v.k, h = v.h, E = v.E, j = v.group;
+  const int* ids = at<int>(v, v.rank, v.off.ids);
+  const A* wts = at<A>(v, v.rank, v.off.w);
+  const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
+  int c0, c1;
+  col_shard(h, m, v.tp_rank, &c0, &c1);
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long tl = gw; tl < v.T; tl += nwarps) {
+    int e = 0, key = 0x7fffffff, pos = 0;
+    A w = (A)0;
+    if (lane < k) {
+      const size_t si = (size_t)tl * k + lane;
+      e = ids[si];
+      w = wts[si];
+      pos = slot_pos[si];
+      const int d = home_of(e, n, E);
+      key = (j - d - 1 + n) % n;  // arrival order (j-1, j-2, ..., j)
+    }
+    // rank of this slot in (arrival key, expert) order
+    int rk = 0;
+    for (int o = 0; o < k; ++o) {
+      const int ok = __shfl_sync(0xffffffffu, key, o);
+      const int oe = __shfl_sync(0xffffffffu, e, o);
+      rk += (ok < key || (ok == key && oe < e)) ? 1 : 0;
+    }
+    if (lane < k) {
+      s_pos[warp][rk] = pos;
+      s_src[warp][rk] = home_of(e, n, E) * m;
+      s_w[warp][rk] = w;
+    }
+    __syncwarp();
+    for (int c = c0 + lane * V; c < c1; c += 32 * V) {
+      A acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = (A)0;
+      for (int s = 0; s < k; ++s) {
+        const size_t off = (size_t)s_pos[warp][s] * h + c;
+        const int r0 = s_src[warp][s];
+        A red[V];
+        if constexpr (VEC) {
+          uint4 raw = ld_v4(at<T>(v, r0, v.off.partial) + off);
+          const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int q = 0; q < V; ++q) red[q] = to_acc(pv[q]);
+          for (int tt = 1; tt < m; ++tt) {
+            uint4 r2 = ld_v4(at<T>(v, r0 + tt, v.off.partial) + off);
+            const T* p2 = reinterpret_cast<const T*>(&r2);
+#pragma unroll
+            for (int q = 0; q < V; ++q) red[q] = add_rn(red[q], to_acc(p2[q]));
+          }
+        } else {
+          red[0] = to_acc(at<T>(v, r0, v.off.partial)[off]);
+          for (int tt = 1; tt < m; ++tt)
+            red[0] = add_rn(red[0], to_acc(at<T>(v, r0 + tt, v.off.partial)[off]));
+        }
+        const A ws = s_w[warp][s];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(ws, red[q]));
+      }
+      // final intra-group all-gather: push the shard to every TP rank
+      for (int tt = 0; tt < m; ++tt) {
+        T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)tl * h + c;
+        if constexpr (VEC) {
+          T outv[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) outv[q] = from_acc<T>(acc[q]);
+          st_v4(y, *reinterpret_cast<uint4*>(outv));
+        } else {
+          y[0] = from_acc<T>(acc[0]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int DT>
+static void launch_combine_dt(const DevView& v, int blocks, cudaStream_t s) {
+  int c0, c1;
+  col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
+  const bool vec = ((size_t)c0 * v.elt) % 16 == 0 && ((size_t)(c1 - c0) * v.elt) % 16 == 0 &&
+                   ((size_t)v.h * v.elt) % 16 == 0;
+  if (vec) k_combine<DT, true><<<blocks, 256, 0, s>>>(v);
+  else k_combine<DT, false><<<blocks, 256, 0, s>>>(v);
+}
+
+int launch_combine(const DevView& v, cudaStream_t s) {
+  if (v.T == 0) return MX_OK;
+  if (v.k > MX_KMAX) return MX_ERR_UNSUPPORTED;
+  long long blocks = (v.T + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  switch (v.elt) {
+    case 8: launch_combine_dt<MX_F64>(v, (int)blocks, s); break;
+    case 4: launch_combine_dt<MX_F32>(v, (int)blocks, s); break;
+    default: launch_combine_dt<MX_BF16>(v, (int)blocks, s);
+  }
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // namespace mx

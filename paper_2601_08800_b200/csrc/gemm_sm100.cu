@@ -1,0 +1,448 @@
+// gemm_sm100.cu -- K3: persistent grouped GEMM on 5th-gen tensor cores.
+//
+// D[rows of group g] = A[rows of g] . B_g^T, bf16 operands, fp32 accumulate
+// in TMEM, for the expert FFN (the reference's _partial_expert_outputs
+// stand-in, sim:535-562, made a real TP-sharded SwiGLU):
+//   GEMM1  A = received rows [S_d, h],  B = w13_e [2*I/m, h] -> SwiGLU
+//          epilogue (silu(gate) * up, bf16) -> act [S_d, I/m]
+//   GEMM2  A = act [S_d, I/m],          B = w2_e [h, I/m]    -> TP partial
+// Groups (= experts of this host) are contiguous row segments of A/D.
+//
+// Structure (one CTA per SM, persistent static tile schedule):
+//   warp 0  TMA producer   cp.async.bulk.tensor 2D, 128B swizzle, mbarriers
+//   warp 1  MMA issuer     tcgen05.mma.cta_group::1.kind::f16, M=128 N=BN K=16
+//   warp 2  TMEM owner     tcgen05.alloc / dealloc (2 x BN fp32 columns)
+//   warps 4-7 epilogue     tcgen05.ld 32x32b -> regs -> (SwiGLU) -> global
+// Double-buffered TMEM accumulators let the epilogue of tile i overlap the
+// MMAs of tile i+1; a STAGES-deep smem ring overlaps TMA with MMA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "mx_internal.cuh"
+
+namespace mx {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B rows: one SWIZZLE_128B atom wide
+constexpr int NUM_THREADS = 256;
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row atoms of
+// 1024 B stacked along M/N (SBO = 1024 B), sm100 version bits = 1.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);  // start address   [0,14)
+  d |= (uint64_t)(16 >> 4) << 16;          // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO             [32,46)
+  d |= (uint64_t)1 << 46;                  // version = 1     [46,48)
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B    [61,64)
+  return d;
+}
+// Instruction descriptor, kind::f16: D f32, A/B bf16, both K-major.
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t idesc_bf16() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+struct Args {
+  void* D;
+  const int32_t* offs;
+  const int32_t* cnts;
+  const int32_t* b_index;
+  int G, N, K, ldd, out_f32;
+  long long M_cap;
+};
+
+// Tile t -> (group, m-block, n-block) through the per-group tile prefix.
+__device__ __forceinline__ void decode_tile(int t, const int* s_tstart, int G, int nN, int* g,
+                                            int* mb, int* nb) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_tstart[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const int r = t - s_tstart[lo];
+  *g = lo;
+  *mb = r / nN;
+  *nb = r % nN;
+}
+
+template <int BN, bool SWIGLU>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
+               const __grid_constant__ CUtensorMap map_b, Args args) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_tstart[MX_EMAX + 1];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = args.G, nN = args.N / BN, kblocks = args.K / BK;
+
+  // per-group tile prefix (G <= MX_EMAX)
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int g = 0; g < G; ++g) {
+      s_tstart[g] = run;
+      run += ((args.cnts[g] + BM - 1) / BM) * nN;
+    }
+    s_tstart[G] = run;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const int total_tiles = s_tstart[G];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int g, mb, nb;
+        decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+        const int a_row = args.offs[g] + mb * BM;
+        const int bg = args.b_index ? args.b_index[g] : g;
+        const int b_row = bg * args.N + nb * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * BK, a_row);
+          tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * BK, b_row);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer (single thread)
+      constexpr uint32_t idesc = idesc_bf16<BN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // +32 B per K=16 step inside the 128 B swizzle atom (>>4 -> +2)
+            mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot when the MMAs retire
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: thread = accumulator row (TMEM lane)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int g, mb, nb;
+      decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+      const int cnt = args.cnts[g];
+      const int r_local = mb * BM + row_in_tile;
+      const bool valid = r_local < cnt;
+      const long long row = (long long)args.offs[g] + r_local;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (SWIGLU) {
+        // tile columns [0, BN/2) = gate, [BN/2, BN) = up (w13 interleave)
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.D) + row * args.ldd + nb * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t gr[32], ur[32];
+          tmem_ld32(tbase + c, gr);
+          tmem_ld32(tbase + BN / 2 + c, ur);
+          tmem_wait_ld();
+          if (valid) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float a0 = silu(__uint_as_float(gr[2 * i])) * __uint_as_float(ur[2 * i]);
+              const float a1 = silu(__uint_as_float(gr[2 * i + 1])) * __uint_as_float(ur[2 * i + 1]);
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+              packed[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          if (valid) {
+            if (args.out_f32) {
+              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.D) + row * args.ldd +
+                                                      nb * BN + c);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                     __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+            } else {
+              uint32_t packed[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                __nv_bfloat162 b2 =
+                    __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                packed[i] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.D) +
+                                                    row * args.ldd + nb * BN + c);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* base, long long rows, int cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return MX_ERR_CUDA; }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%d", (int)r, rows, cols);
+    return MX_ERR_CUDA;
+  }
+  return MX_OK;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool SWIGLU>
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, long long max_tiles,
+                  cudaStream_t s) {
+  auto kern = k_grouped_gemm<BN, SWIGLU>;
+  static bool attr = false;
+  if (!attr) {
+    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+    attr = true;
+  }
+  long long grid = sm_count();
+  if (max_tiles < grid) grid = max_tiles < 1 ? 1 : max_tiles;
+  kern<<<(int)grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ma, mb, a);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // namespace gemm
+
+int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,
+                 const int32_t* cnts, const int32_t* b_index, int G, long long M_total,
+                 long long M_cap, int N, int K, int swiglu, cudaStream_t s) {
+  using namespace gemm;
+  if (G < 1 || G > MX_EMAX) { set_error("grouped_gemm: G=%d outside [1, %d]", G, MX_EMAX); return MX_ERR_UNSUPPORTED; }
+  if (K % BK != 0 || N % 128 != 0) { set_error("grouped_gemm: K %% 64 and N %% 128 must be 0 (K=%d N=%d)", K, N); return MX_ERR_UNSUPPORTED; }
+  if (swiglu && (N % 256 != 0 || out_dtype != MX_BF16)) { set_error("grouped_gemm: SwiGLU needs N %% 256 == 0 and bf16 out"); return MX_ERR_UNSUPPORTED; }
+  if (out_dtype != MX_BF16 && out_dtype != MX_F32) { set_error("grouped_gemm: out dtype"); return MX_ERR_UNSUPPORTED; }
+  if (M_cap < 1) return MX_OK;
+  const int bn = (N % 256 == 0) ? 256 : 128;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, M_cap, K, BM);
+  if (rc) return rc;
+  // B rows: every group's N rows (b_index may address any of them)
+  long long b_rows = (long long)G * N;
+  rc = make_map(&mb, B, b_rows, K, bn);
+  if (rc) return rc;
+  Args a{};
+  a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index;
+  a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
+  a.M_cap = M_cap;
+  // upper bound on tiles (host does not know the per-group counts)
+  const long long max_tiles = ((M_total + BM - 1) / BM + G) * (N / bn);
+  if (bn == 256) return swiglu ? launch<256, true>(ma, mb, a, max_tiles, s)
+                               : launch<256, false>(ma, mb, a, max_tiles, s);
+  return launch<128, false>(ma, mb, a, max_tiles, s);
+}
+
+// Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.
+int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, cudaStream_t s) {
+  const int e0 = first_expert(v.group, v.n, v.E), e1 = first_expert(v.group + 1, v.n, v.E);
+  const int El = e1 - e0;
+  if (El == 0) return MX_OK;
+  const int32_t* offs = at<int32_t>(v, v.rank, v.off.exp_off) + e0;
+  const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
+  int rc = grouped_gemm(at<char>(v, v.rank, v.off.recv), w13, at<char>(v, v.rank, v.off.act),
+                        MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, 2 * v.I_t, v.h, 1, s);
+  if (rc) return rc;
+  return grouped_gemm(at<char>(v, v.rank, v.off.act), w2, at<char>(v, v.rank, v.off.partial),
+                      MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s);
+}
+
+}  // namespace mx

@@ -1,0 +1,150 @@
+// misc.cu -- weight packing and the independent dense GPU reference used by
+// the API's moe_oracle mirror (sim:302-310).  Neither is on the fused path.
+#include "mx_internal.cuh"
+
+namespace mx {
+
+// w13[e][256*b + r] = gate[e][128*b + r] (r < 128), up[e][128*b + r-128]
+__global__ void k_pack_w13(const __nv_bfloat16* gate, const __nv_bfloat16* up, __nv_bfloat16* w13,
+                           int E_l, int I_t, int h) {
+  const long long rows = (long long)E_l * 2 * I_t;
+  for (long long rr = blockIdx.x; rr < rows; rr += gridDim.x) {
+    const int e = (int)(rr / (2 * I_t)), r = (int)(rr % (2 * I_t));
+    const int b = r / 256, q = r % 256;
+    const __nv_bfloat16* src = (q < 128 ? gate : up) + ((size_t)e * I_t + b * 128 + (q & 127)) * h;
+    __nv_bfloat16* dst = w13 + (size_t)rr * h;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) dst[c] = src[c];
+  }
+}
+
+// One CTA per token; slots visited in ascending expert id (sim:306-309).
+template <int DT>
+__global__ void k_dense_affine(int h, int k, const typename Elt<DT>::T* x, const int32_t* ids,
+                               const typename Elt<DT>::Acc* w, const typename Elt<DT>::Acc* sc,
+                               const typename Elt<DT>::Acc* bi, typename Elt<DT>::T* y) {
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  const int t = blockIdx.x;
+  __shared__ int s_ord[MX_KMAX];
+  if (threadIdx.x < k) {
+    const int e = ids[(size_t)t * k + threadIdx.x];
+    int rk = 0;
+    for (int o = 0; o < k; ++o) rk += ids[(size_t)t * k + o] < e ? 1 : 0;
+    s_ord[rk] = threadIdx.x;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    const A xv = to_acc(x[(size_t)t * h + c]);
+    A acc = (A)0;
+    for (int s = 0; s < k; ++s) {
+      const int i = s_ord[s];
+      const int e = ids[(size_t)t * k + i];
+      acc = add_rn(acc, mul_rn(w[(size_t)t * k + i], add_rn(mul_rn(sc[e], xv), bi[e])));
+    }
+    y[(size_t)t * h + c] = from_acc<T>(acc);
+  }
+}
+
+__global__ void k_dense_swiglu(int h, int k, int I, const __nv_bfloat16* x, const int32_t* ids,
+                               const float* w, const __nv_bfloat16* wg, const __nv_bfloat16* wu,
+                               const __nv_bfloat16* wd, float* y) {
+  extern __shared__ float s_buf[];  // x row [h] + act [I]
+  float* s_x = s_buf;
+  float* s_a = s_buf + h;
+  __shared__ int s_ord[MX_KMAX];
+  const int t = blockIdx.x;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) s_x[c] = __bfloat162float(x[(size_t)t * h + c]);
+  if (threadIdx.x < k) {
+    const int e = ids[(size_t)t * k + threadIdx.x];
+    int rk = 0;
+    for (int o = 0; o < k; ++o) rk += ids[(size_t)t * k + o] < e ? 1 : 0;
+    s_ord[rk] = threadIdx.x;
+  }
+  for (int c = threadIdx.x; c < h; c += blockDim.x) y[(size_t)t * h + c] = 0.f;
+  __syncthreads();
+  for (int s = 0; s < k; ++s) {
+    const int i = s_ord[s];
+    const int e = ids[(size_t)t * k + i];
+    const float ws = w[(size_t)t * k + i];
+    for (int r = threadIdx.x; r < I; r += blockDim.x) {
+      const __nv_bfloat16* g = wg + ((size_t)e * I + r) * h;
+      const __nv_bfloat16* u = wu + ((size_t)e * I + r) * h;
+      float ga = 0.f, ua = 0.f;
+      for (int c = 0; c < h; ++c) {
+        ga = fmaf(s_x[c], __bfloat162float(g[c]), ga);
+        ua = fmaf(s_x[c], __bfloat162float(u[c]), ua);
+      }
+      const float a = ga / (1.f + expf(-ga)) * ua;
+      s_a[r] = __bfloat162float(__float2bfloat16_rn(a));  // product rounding point
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      const __nv_bfloat16* d = wd + ((size_t)e * h + c) * I;
+      float o = 0.f;
+      for (int r = 0; r < I; ++r) o = fmaf(s_a[r], __bfloat162float(d[r]), o);
+      y[(size_t)t * h + c] += ws * o;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace mx
+
+using namespace mx;
+
+extern "C" {
+
+int mx_swiglu_pack_w13(const void* gate, const void* up, void* w13, int E_l, int I_t, int h,
+                       void* stream) {
+  if (I_t % 128 != 0) { set_error("I/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED; }
+  const long long rows = (long long)E_l * 2 * I_t;
+  if (rows == 0) return MX_OK;
+  k_pack_w13<<<(int)(rows < 65535 ? rows : 65535), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(gate), static_cast<const __nv_bfloat16*>(up),
+      static_cast<__nv_bfloat16*>(w13), E_l, I_t, h);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+int mx_dense_moe(int T, int h, int E, int k, int act_dtype, int expert_kind, int inter,
+                 const void* x, const int32_t* ids, const void* weights, const void* scales,
+                 const void* biases, const void* w_gate, const void* w_up, const void* w_down,
+                 void* y, void* stream) {
+  (void)E;
+  if (T == 0) return MX_OK;
+  if (k > MX_KMAX) { set_error("top_k exceeds %d", MX_KMAX); return MX_ERR_UNSUPPORTED; }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (expert_kind == MX_EXPERT_AFFINE) {
+    switch (act_dtype) {
+      case MX_F64:
+        k_dense_affine<MX_F64><<<T, 128, 0, s>>>(h, k, (const double*)x, ids, (const double*)weights,
+                                                 (const double*)scales, (const double*)biases, (double*)y);
+        break;
+      case MX_F32:
+        k_dense_affine<MX_F32><<<T, 128, 0, s>>>(h, k, (const float*)x, ids, (const float*)weights,
+                                                 (const float*)scales, (const float*)biases, (float*)y);
+        break;
+      default:
+        k_dense_affine<MX_BF16><<<T, 128, 0, s>>>(h, k, (const __nv_bfloat16*)x, ids,
+                                                  (const float*)weights, (const float*)scales,
+                                                  (const float*)biases, (__nv_bfloat16*)y);
+    }
+  } else {
+    if (act_dtype != MX_BF16) { set_error("dense SwiGLU reference takes bf16"); return MX_ERR_UNSUPPORTED; }
+    const size_t smem = (size_t)(h + inter) * 4;
+    if (smem > 200 * 1024) { set_error("dense SwiGLU reference: h+I too large"); return MX_ERR_UNSUPPORTED; }
+    static bool attr = false;
+    if (!attr) {
+      MX_CUDA(cudaFuncSetAttribute(k_dense_swiglu, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_dense_swiglu<<<T, 256, smem, s>>>(h, k, inter, (const __nv_bfloat16*)x, ids,
+                                        (const float*)weights, (const __nv_bfloat16*)w_gate,
+                                        (const __nv_bfloat16*)w_up, (const __nv_bfloat16*)w_down,
+                                        (float*)y);
+  }
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,167 @@
+// mx_internal.cuh -- shared types, heap layout and PTX helpers.
+//
+// Every rank owns one symmetric heap (identical offsets on all ranks), so a
+// kernel reaches buffer B of rank r as heap[r] + off.B.  In SPMD mode
+// heap[r] for r != self is a CUDA-IPC mapping of the peer's heap (NVLink 5
+// through NVSwitch); in emulated mode all heaps live on one device.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/mixserve_b200.h"
+
+#define MX_MAXW 64         // max ranks in one cluster view
+#define MX_CHUNK 128       // tokens per router chunk (one CTA)
+#define MX_KMAX 32         // max top-k handled by the kernels
+#define MX_EMAX 1024       // max experts
+#define MX_NMAX 64         // max groups
+
+namespace mx {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define MX_CUDA(call)                                                      \
+  do {                                                                     \
+    cudaError_t _e = (call);                                               \
+    if (_e != cudaSuccess) return ::mx::cuda_fail(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+#define MX_LAUNCH_CHECK() MX_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- layout
+struct Offsets {
+  size_t flags;       // uint64 [MX_MAXW]   barrier epochs written by peers
+  size_t cnt_all;     // int32 [n][E]       pushed by every group (symmetric)
+  size_t recv;        // act [cap][h]       written by peers (dispatch)
+  size_t partial;     // act [cap][h]       read by peers (combine)
+  size_t y;           // act [T][h]         written by TP peers (final AG)
+  size_t act;         // bf16 [cap][I_t]    SwiGLU activation (local)
+  size_t ids;         // int32 [T][k]
+  size_t w;           // AccT [T][k]
+  size_t slot_pos;    // int32 [T][k]
+  size_t slot_tm;     // int32 [T][k]
+  size_t slot_rank;   // int32 [T][k]  rank among chunk tokens of the expert
+  size_t slot_tmr;    // int32 [T][k]  token-major rank inside the chunk/host
+  size_t chunk_hist;  // int32 [C][E]  -> exclusive chunk base after route
+  size_t chunk_host;  // int32 [C][n]  -> exclusive chunk base after route
+  size_t exp_off;     // int32 [E]
+  size_t exp_cnt;     // int32 [E]
+  size_t grp_off;     // int32 [n][E]
+  size_t send;        // int32 [n][n]
+  size_t tm_off;      // int32 [n][n]
+  size_t host_rows;   // int32 [n]
+  size_t counters;    // int32 [16]
+  size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
+  size_t total;
+};
+
+struct DevView {
+  int rank, group, tp_rank, n, m, W;
+  int T, h, E, k, I_t, C;
+  int elt;            // bytes per hidden element on the wire
+  int renorm;
+  long long cap;
+  Offsets off;
+  char* heap[MX_MAXW];
+};
+
+template <class T>
+__host__ __device__ __forceinline__ T* at(const DevView& v, int r, size_t off) {
+  return reinterpret_cast<T*>(v.heap[r] + off);
+}
+
+__host__ __device__ __forceinline__ int home_of(int e, int n, int E) {
+  return (int)(((long long)e * n) / E);  // sim:210-212
+}
+// first expert hosted on group d: smallest e with e*n//E == d
+__host__ __device__ __forceinline__ int first_expert(int d, int n, int E) {
+  return (int)(((long long)d * E + n - 1) / n);
+}
+// array_split column shards (sim:317-323)
+__host__ __device__ __forceinline__ void col_shard(int h, int m, int t, int* c0, int* c1) {
+  int base = h / m, rem = h % m;
+  *c0 = t * base + (t < rem ? t : rem);
+  *c1 = *c0 + base + (t < rem ? 1 : 0);
+}
+
+// ---------------------------------------------------------------- PTX
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w) : "memory");
+}
+
+// ---------------------------------------------------------------- dtypes
+template <int DT> struct Elt;
+template <> struct Elt<MX_F64> { using T = double; using Acc = double; static constexpr int V = 2; };
+template <> struct Elt<MX_F32> { using T = float; using Acc = float; static constexpr int V = 4; };
+template <> struct Elt<MX_BF16> { using T = __nv_bfloat16; using Acc = float; static constexpr int V = 8; };
+
+__device__ __forceinline__ double to_acc(double x) { return x; }
+__device__ __forceinline__ float to_acc(float x) { return x; }
+__device__ __forceinline__ float to_acc(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <class T> __device__ __forceinline__ T from_acc(double x);
+template <class T> __device__ __forceinline__ T from_acc(float x);
+template <> __device__ __forceinline__ double from_acc<double>(double x) { return x; }
+template <> __device__ __forceinline__ float from_acc<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+// Uncontracted arithmetic: the f64 path reproduces the reference's numpy
+// association exactly (no FMA fusion), sim:433-441 / sim:506-520.
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
+// ---------------------------------------------------------------- host plan
+struct Comm;
+struct Plan;
+
+// kernels (launchers live next to their kernels)
+int launch_route(const DevView& v, const float* logits, const int32_t* ids,
+                 const void* w, cudaStream_t s);
+int launch_layout(const DevView& v, cudaStream_t s);
+int launch_dispatch(const DevView& v, const void* x, cudaStream_t s);
+int launch_expert_affine(const DevView& v, const void* scales, const void* biases,
+                         cudaStream_t s);
+int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2,
+                         cudaStream_t s);
+int launch_combine(const DevView& v, cudaStream_t s);
+int launch_barrier(const DevView& v, unsigned long long epoch, cudaStream_t s);
+int launch_baseline_dispatch_pack(const DevView& v, const void* x, void* send,
+                                  int32_t* counts, cudaStream_t s);
+int launch_baseline_dispatch_unpack(const DevView& v, const void* recv, cudaStream_t s);
+int launch_baseline_combine_pack(const DevView& v, void* send, int32_t* counts,
+                                 cudaStream_t s);
+int launch_baseline_combine_unpack(const DevView& v, const void* recv, void* y,
+                                   cudaStream_t s);
+int grouped_gemm(const void* A, const void* B, void* D, int out_dtype,
+                 const int32_t* offs, const int32_t* cnts, const int32_t* b_index,
+                 int G, long long M_total, long long M_cap, int N, int K, int swiglu,
+                 cudaStream_t s);
+
+}  // namespace mx

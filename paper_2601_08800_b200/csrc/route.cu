@@ -1,0 +1,349 @@
+// route.cu -- K1: fused top-k gate + per-expert counting + stable ranks +
+// chunk prefix sums, and the layout pass that turns them into expert-major
+// and token-major slot positions.
+//
+// Replaces the reference's O(T*k) Python loops:
+//   RouterSpec (sim:143-186)            -> ids/weights (or the fused gate)
+//   build_routing_table (sim:236-251)   -> token-major table index (slot_tm)
+//   _slot_rows_from (sim:326-327)       -> send counts S[j][d] + tm offsets
+//   _expert_rows (sim:528-532)          -> expert-major row (slot_pos)
+//
+// Order contracts (bit-exact with the reference):
+//   host d's token-major table = all (token, expert) with home(expert)=d,
+//   sorted by (global token, expert); expert-major = experts ascending,
+//   inside an expert tokens ascending.  Groups own contiguous token blocks,
+//   so both orders decompose into per-group contiguous sub-blocks whose
+//   offsets only need the [n][E] count matrix.
+#include "mx_internal.cuh"
+
+namespace mx {
+
+// One CTA per chunk of MX_CHUNK tokens of this rank's group.
+template <class WT>
+__global__ void __launch_bounds__(256)
+k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__ ids_in,
+        const WT* __restrict__ w_in) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int T = v.T, E = v.E, k = v.k, n = v.n;
+  const int c = blockIdx.x, t0 = c * MX_CHUNK;
+  const int nt = min(MX_CHUNK, T - t0);
+  int* s_ids = reinterpret_cast<int*>(smem);                      // [CHUNK*k]
+  unsigned* s_mask = reinterpret_cast<unsigned*>(s_ids + MX_CHUNK * k);  // [E][4]
+  int* s_hc = reinterpret_cast<int*>(s_mask + E * 4);             // [CHUNK][n]
+  __shared__ int s_last;
+
+  int* ids = at<int>(v, v.rank, v.off.ids);
+  WT* w = at<WT>(v, v.rank, v.off.w);
+  int* slot_rank = at<int>(v, v.rank, v.off.slot_rank);
+  int* slot_tmr = at<int>(v, v.rank, v.off.slot_tmr);
+  int* chunk_hist = at<int>(v, v.rank, v.off.chunk_hist);
+  int* chunk_host = at<int>(v, v.rank, v.off.chunk_host);
+  int* err = at<int>(v, v.rank, v.off.err);
+  int* counters = at<int>(v, v.rank, v.off.counters);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+
+  for (int i = threadIdx.x; i < E * 4; i += blockDim.x) s_mask[i] = 0;
+  for (int i = threadIdx.x; i < MX_CHUNK * n; i += blockDim.x) s_hc[i] = 0;
+
+  if (logits != nullptr) {
+    // ---- fused softmax + top-k: one warp per token, lane owns experts
+    //      e = 128*i + 4*lane + q (128-bit coalesced loads when aligned).
+    const bool vec = (E % 4) == 0;
+    for (int tl = warp; tl < nt; tl += nw) {
+      const float* row = logits + (size_t)(t0 + tl) * E;
+      float val[MX_EMAX / 32];
+#pragma unroll
+      for (int i = 0; i < MX_EMAX / 128; ++i) {
+        const int e0 = 128 * i + 4 * lane;
+        if (vec && e0 < E) {
+          float4 f = __ldg(reinterpret_cast<const float4*>(row + e0));
+          val[4 * i] = f.x; val[4 * i + 1] = f.y; val[4 * i + 2] = f.z; val[4 * i + 3] = f.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            val[4 * i + q] = (e0 + q < E) ? __ldg(row + e0 + q) : -INFINITY;
+        }
+      }
+      unsigned taken = 0;
+      int my_e = 0;
+      float my_v = 0.f;
+      for (int r = 0; r < k; ++r) {
+        float bv = -INFINITY;
+        int be = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < MX_EMAX / 32; ++i) {
+          const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+          const bool ok = e < E && !((taken >> i) & 1u);
+          if (ok && (val[i] > bv || (val[i] == bv && e < be))) { bv = val[i]; be = e; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          int oe = __shfl_xor_sync(0xffffffffu, be, o);
+          if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+        }
+        if (((be & 127) >> 2) == lane) taken |= 1u << (4 * (be >> 7) + (be & 3));
+        if (lane == r) { my_e = be; my_v = bv; }
+      }
+      const float mx = __shfl_sync(0xffffffffu, my_v, 0);  // top-1 = row max
+      float ex = (lane < k) ? expf(my_v - mx) : 0.f;
+      float denom;
+      if (v.renorm) {
+        denom = ex;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+      } else {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < MX_EMAX / 32; ++i) {
+          const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+          if (e < E) s += expf(val[i] - mx);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        denom = s;
+      }
+      if (lane < k) {
+        const size_t si = (size_t)(t0 + tl) * k + lane;
+        ids[si] = my_e;
+        w[si] = (WT)(ex / denom);
+        s_ids[tl * k + lane] = my_e;
+      }
+    }
+  } else {
+    // ---- explicit routing (RouterSpec ids/weights, sim:143-166)
+    for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+      const size_t si = (size_t)t0 * k + i;
+      int e = ids_in[si];
+      if (e < 0 || e >= E) { atomicOr(err + 1, 1); e = 0; }
+      ids[si] = e;
+      w[si] = w_in[si];
+      s_ids[i] = e;
+    }
+  }
+  __syncthreads();
+
+  // ---- per-expert token bitmaps of this chunk
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int e = s_ids[i], tl = i / k;
+    atomicOr(&s_mask[e * 4 + (tl >> 5)], 1u << (tl & 31));
+  }
+  __syncthreads();
+
+  // ---- stable rank of each slot among the chunk's tokens of its expert,
+  //      and per-token host counts (token-major table order).
+  if (threadIdx.x < nt) {
+    const int tl = threadIdx.x;
+    for (int i = 0; i < k; ++i) {
+      const int e = s_ids[tl * k + i];
+      const int d = home_of(e, n, E);
+      int rk = 0;
+      for (int wd = 0; wd < (tl >> 5); ++wd) rk += __popc(s_mask[e * 4 + wd]);
+      rk += __popc(s_mask[e * 4 + (tl >> 5)] & ((1u << (tl & 31)) - 1u));
+      int within = 0;  // experts of this token on host d with a smaller id
+      for (int i2 = 0; i2 < k; ++i2) {
+        const int e2 = s_ids[tl * k + i2];
+        within += (e2 < e && home_of(e2, n, E) == d) ? 1 : 0;
+      }
+      const size_t si = (size_t)(t0 + tl) * k + i;
+      slot_rank[si] = rk;
+      slot_tmr[si] = within;
+      s_hc[tl * n + d] += 1;
+    }
+  }
+  __syncthreads();
+  // exclusive scan of host counts over the chunk's tokens (4 per lane)
+  for (int d = warp; d < n; d += nw) {
+    int a[4], run = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tl = 4 * lane + q;
+      a[q] = (tl < nt) ? s_hc[tl * n + d] : 0;
+      run += a[q];
+    }
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int ex = incl - run;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tl = 4 * lane + q;
+      if (tl < MX_CHUNK) s_hc[tl * n + d] = ex;
+      ex += a[q];
+    }
+    if (lane == 31) chunk_host[c * n + d] = incl;
+  }
+  __syncthreads();
+  if (threadIdx.x < nt) {
+    const int tl = threadIdx.x;
+    for (int i = 0; i < k; ++i) {
+      const int e = s_ids[tl * k + i];
+      const size_t si = (size_t)(t0 + tl) * k + i;
+      slot_tmr[si] += s_hc[tl * n + home_of(e, n, E)];
+    }
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    chunk_hist[c * E + e] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
+                            __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
+  }
+
+  // ---- last CTA: exclusive chunk prefix per expert / host, totals, publish
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counters, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int C = gridDim.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int cc = 0; cc < C; ++cc) {
+      const int hv = __ldcg(chunk_hist + cc * E + e);
+      chunk_hist[cc * E + e] = run;
+      run += hv;
+    }
+    // publish this group's count row to every rank (peer stores in SPMD)
+    for (int r = 0; r < v.W; ++r) at<int>(v, r, v.off.cnt_all)[v.group * E + e] = run;
+  }
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    int run = 0;
+    for (int cc = 0; cc < C; ++cc) {
+      const int hv = __ldcg(chunk_host + cc * n + d);
+      chunk_host[cc * n + d] = run;
+      run += hv;
+    }
+  }
+  if (threadIdx.x == 0) counters[0] = 0;
+}
+
+// Offsets of the layout from the gathered [n][E] count matrix (one CTA).
+__global__ void __launch_bounds__(1024) k_layout_meta(DevView v) {
+  const int n = v.n, E = v.E;
+  const int* cnt = at<int>(v, v.rank, v.off.cnt_all);
+  int* exp_off = at<int>(v, v.rank, v.off.exp_off);
+  int* exp_cnt = at<int>(v, v.rank, v.off.exp_cnt);
+  int* grp_off = at<int>(v, v.rank, v.off.grp_off);
+  int* send = at<int>(v, v.rank, v.off.send);
+  int* tm_off = at<int>(v, v.rank, v.off.tm_off);
+  int* host_rows = at<int>(v, v.rank, v.off.host_rows);
+  int* err = at<int>(v, v.rank, v.off.err);
+  __shared__ int s_scan[MX_EMAX];
+  __shared__ int s_tot[MX_EMAX];
+  __shared__ int s_send[MX_NMAX * MX_NMAX];
+  const int e = threadIdx.x;
+  int tot = 0;
+  if (e < E) {
+    for (int j = 0; j < n; ++j) {
+      grp_off[j * E + e] = tot;  // rows of groups j' < j for expert e
+      tot += cnt[j * E + e];
+    }
+    exp_cnt[e] = tot;
+  }
+  s_tot[e] = tot;
+  s_scan[e] = tot;
+  __syncthreads();
+  for (int o = 1; o < MX_EMAX; o <<= 1) {
+    const int y = (e >= o) ? s_scan[e - o] : 0;
+    __syncthreads();
+    s_scan[e] += y;
+    __syncthreads();
+  }
+  if (e < E) {
+    const int f = first_expert(home_of(e, n, E), n, E);
+    exp_off[e] = (s_scan[e] - tot) - (s_scan[f] - s_tot[f]);
+  }
+  // S[j][d]: slots of group j's tokens hosted on group d
+  for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
+    const int j = jd / n, d = jd % n;
+    const int e0 = first_expert(d, n, E), e1 = first_expert(d + 1, n, E);
+    int s = 0;
+    for (int x = e0; x < e1; ++x) s += cnt[j * E + x];
+    s_send[jd] = s;
+    send[jd] = s;
+  }
+  __syncthreads();
+  for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
+    const int j = jd / n, d = jd % n;
+    int s = 0;
+    for (int j2 = 0; j2 < j; ++j2) s += s_send[j2 * n + d];
+    tm_off[jd] = s;
+  }
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    int s = 0;
+    for (int j = 0; j < n; ++j) s += s_send[j * n + d];
+    host_rows[d] = s;
+    if ((long long)s > v.cap) atomicMax(err + 0, s);  // CapacityError (sim:346-351)
+  }
+}
+
+// Final slot positions: expert-major row in the host's RECV buffer and the
+// index in the host's token-major routing table.
+__global__ void k_slotpos(DevView v) {
+  const int n = v.n, E = v.E, k = v.k;
+  const int* ids = at<int>(v, v.rank, v.off.ids);
+  const int* slot_rank = at<int>(v, v.rank, v.off.slot_rank);
+  const int* slot_tmr = at<int>(v, v.rank, v.off.slot_tmr);
+  const int* chunk_hist = at<int>(v, v.rank, v.off.chunk_hist);
+  const int* chunk_host = at<int>(v, v.rank, v.off.chunk_host);
+  const int* exp_off = at<int>(v, v.rank, v.off.exp_off);
+  const int* grp_off = at<int>(v, v.rank, v.off.grp_off);
+  const int* tm_off = at<int>(v, v.rank, v.off.tm_off);
+  int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
+  int* slot_tm = at<int>(v, v.rank, v.off.slot_tm);
+  int* err = at<int>(v, v.rank, v.off.err);
+  const long long total = (long long)v.T * k;
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < total;
+       s += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(s / k);
+    const int e = ids[s];
+    const int d = home_of(e, n, E);
+    const int c = t / MX_CHUNK;
+    const long long pos = (long long)exp_off[e] + grp_off[v.group * E + e] +
+                          chunk_hist[c * E + e] + slot_rank[s];
+    const int tm = tm_off[v.group * n + d] + chunk_host[c * n + d] + slot_tmr[s];
+    if (pos >= v.cap) atomicOr(err + 3, 1);
+    slot_pos[s] = (int)pos;
+    slot_tm[s] = tm;
+  }
+}
+
+int launch_route(const DevView& v, const float* logits, const int32_t* ids,
+                 const void* w, cudaStream_t s) {
+  const int C = (v.T + MX_CHUNK - 1) / MX_CHUNK;
+  if (C == 0) return MX_OK;
+  const size_t smem = (size_t)MX_CHUNK * v.k * 4 + (size_t)v.E * 16 + (size_t)MX_CHUNK * v.n * 4;
+  if (v.elt == 8) {
+    static bool attr = false;
+    if (!attr) {
+      MX_CUDA(cudaFuncSetAttribute(k_route<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_route<double><<<C, 256, smem, s>>>(v, logits, ids, static_cast<const double*>(w));
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      MX_CUDA(cudaFuncSetAttribute(k_route<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_route<float><<<C, 256, smem, s>>>(v, logits, ids, static_cast<const float*>(w));
+  }
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+int launch_layout(const DevView& v, cudaStream_t s) {
+  k_layout_meta<<<1, 1024, 0, s>>>(v);
+  MX_LAUNCH_CHECK();
+  const long long total = (long long)v.T * v.k;
+  if (total > 0) {
+    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    k_slotpos<<<blocks, 256, 0, s>>>(v);
+    MX_LAUNCH_CHECK();
+  }
+  return MX_OK;
+}
+
+}  // namespace mx

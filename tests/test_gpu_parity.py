@@ -1,0 +1,288 @@
+"""Parity of the CUDA path (through the C-ABI) against the CPU oracle and the
+reference's frozen outputs.  Runs on a B200 (``-m gpu``)."""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_names, load_golden
+from oracle import mixserve_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _meta(g):
+    return json.loads(str(g["meta"]))
+
+
+def _router(g):
+    from paper_2601_08800_b200 import RouterSpec
+    return RouterSpec.from_arrays(_meta(g)["E"], g["ids"], g["weights"])
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    torch.cuda.set_device(0)
+    from paper_2601_08800_b200 import _native
+    _native.load()
+
+
+# ----------------------------------------------------------------- routing
+@pytest.mark.parametrize("name", golden_names())
+def test_routing_table_bit_exact(name):
+    from paper_2601_08800_b200 import build_routing_table
+    g = load_golden(name)
+    mt = _meta(g)
+    n = mt["n"]
+    tab = build_routing_table(_router(g), n, mt["tokens"] // n)
+    for d in range(n):
+        assert np.array_equal(tab.token[d], g[f"tok_{d}"])
+        assert np.array_equal(tab.expert[d], g[f"exp_{d}"])
+        assert np.array_equal(tab.src[d], g[f"src_{d}"])
+        assert np.array_equal(tab.weight[d], g[f"w_{d}"])
+    ref = orc.Table(g["ids"], g["weights"], n, mt["tokens"] // n, mt["E"])
+    assert np.array_equal(np.asarray(tab.send), ref.send_counts())
+    assert tab.total_slots() == mt["tokens"] * g["ids"].shape[1]
+    # reference Slot objects materialise identically
+    s0 = tab.slots_by_host[0][:3]
+    for i, s in enumerate(s0):
+        assert (s.token, s.expert, s.src_node, s.host_node) == (
+            int(g["tok_0"][i]), int(g["exp_0"][i]), int(g["src_0"][i]), 0)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_expert_major_layout_bit_exact(name):
+    """slot_pos reproduces concat(_expert_rows) (sim:528-532) exactly."""
+    from paper_2601_08800_b200.simcluster import _plan, _route
+    g = load_golden(name)
+    mt = _meta(g)
+    n, m, T = mt["n"], mt["m"], mt["tokens"] // mt["n"]
+    router = _router(g)
+    plan = _plan(n, m, T, mt["h"], mt["E"], g["ids"].shape[1], torch.float64)
+    _route(plan, router)
+    ref = orc.Table(g["ids"], g["weights"], n, T, mt["E"])
+    for d in range(n):
+        # table index of the slot stored at every expert-major row of host d
+        S_d = ref.slots(d)
+        at_row = np.full(S_d, -1)
+        for grp in range(n):
+            v = {k: t.cpu().numpy() for k, t in plan.rank_views(grp * m).items()}
+            sel = (v["ids"].astype(np.int64) * n) // mt["E"] == d
+            at_row[v["slot_pos"][sel]] = v["slot_tm"][sel]
+        assert np.array_equal(at_row, g[f"emajor_{d}"])
+
+
+# ----------------------------------------------------------------- layer
+@pytest.mark.parametrize("name", golden_names())
+def test_fused_layer_f64_bit_exact(name):
+    from paper_2601_08800_b200 import (ExpertSpec, build_cluster, run_moe_block,
+                                       verify_against_oracle)
+    from paper_2601_08800_b200.trace import trace_to_csv
+    g = load_golden(name)
+    mt = _meta(g)
+    cluster = build_cluster(mt["n"], mt["m"])
+    router, experts = _router(g), ExpertSpec.default(mt["E"])
+    y, trace = run_moe_block(cluster, g["x"], router, experts, mode="fused")
+    assert np.array_equal(y, g["y_fused"])          # same association, f64
+    assert trace_to_csv(trace.events) == str(g["trace_csv"])
+    assert verify_against_oracle(y, g["x"], router, experts) <= 1e-9
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_baseline_layer_matches_reference(name):
+    from paper_2601_08800_b200 import ExpertSpec, build_cluster, run_moe_block
+    from paper_2601_08800_b200.trace import trace_to_csv
+    g = load_golden(name)
+    mt = _meta(g)
+    y, trace = run_moe_block(build_cluster(mt["n"], mt["m"]), g["x"], _router(g),
+                             ExpertSpec.default(mt["E"]), mode="baseline")
+    assert np.allclose(y, g["y_baseline"], rtol=1e-9, atol=1e-12)
+    assert trace_to_csv(trace.events) == str(g["trace_baseline_csv"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_dense_gpu_oracle_bit_exact(name):
+    from paper_2601_08800_b200 import ExpertSpec, moe_oracle
+    g = load_golden(name)
+    y = moe_oracle(g["x"], _router(g), ExpertSpec.default(_meta(g)["E"]))
+    assert np.array_equal(y, g["y_oracle"])
+
+
+def test_dispatch_received_rows_bit_exact():
+    from paper_2601_08800_b200 import build_cluster, fused_ag_dispatch
+    g = load_golden("ref_grid_07")
+    mt = _meta(g)
+    n, m, T = mt["n"], mt["m"], mt["tokens"] // mt["n"]
+    xs = [g["x"][j * T:(j + 1) * T] for j in range(n)]
+    received, table, trace = fused_ag_dispatch(build_cluster(n, m), xs, _router(g))
+    ref = orc.Table(g["ids"], g["weights"], n, T, mt["E"])
+    want = orc.dispatch_received(xs, ref)
+    for d in range(n):
+        assert np.array_equal(received[d], want[d])
+
+
+def test_rs_combine_from_oracle_partials():
+    from paper_2601_08800_b200 import build_cluster, fused_rs_combine
+    from paper_2601_08800_b200.simcluster import build_routing_table
+    g = load_golden("ref_grid_05")
+    mt = _meta(g)
+    n, m, T, h, E = mt["n"], mt["m"], mt["tokens"] // mt["n"], mt["h"], mt["E"]
+    ref = orc.Table(g["ids"], g["weights"], n, T, E)
+    xs = [g["x"][j * T:(j + 1) * T] for j in range(n)]
+    parts = orc.partial_affine(orc.dispatch_received(xs, ref), ref,
+                               [e + 1.0 for e in range(E)], [float(e) for e in range(E)],
+                               m, h)
+    table = build_routing_table(_router(g), n, T)
+    ys, _ = fused_rs_combine(build_cluster(n, m), parts, table)
+    assert np.array_equal(np.concatenate(ys), g["y_fused"])
+
+
+def test_capacity_error():
+    from paper_2601_08800_b200 import (CapacityError, RouterSpec, build_cluster,
+                                       fused_ag_dispatch)
+    x = np.random.default_rng(0).standard_normal((8, 8))
+    skew = RouterSpec(4, tuple((0,) for _ in range(8)), tuple((1.0,) for _ in range(8)))
+    with pytest.raises(CapacityError, match="capacity"):
+        fused_ag_dispatch(build_cluster(2, 2), [x[:4], x[4:]], skew, capacity=4)
+
+
+def test_uneven_tokens_raise_strategy_error():
+    from paper_2601_08800_b200 import (ExpertSpec, RouterSpec, StrategyError,
+                                       build_cluster, run_moe_block)
+    x = np.zeros((3, 8))
+    with pytest.raises(StrategyError, match="split evenly"):
+        run_moe_block(build_cluster(2, 1), x, RouterSpec.round_robin(3, 2, 1),
+                      ExpertSpec.default(2))
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+@pytest.mark.parametrize("shape", [(1, 1), (2, 2), (4, 2), (2, 4)])
+def test_fused_layer_low_precision(dtype, tol, shape):
+    from paper_2601_08800_b200 import ExpertSpec, build_cluster, run_moe_block
+    n, m = shape
+    g = load_golden("ref_config_a") if shape == (2, 2) else None
+    rng = np.random.default_rng(11)
+    T_g, h, E, k = 64 * n, 128, 16, 4
+    x = rng.standard_normal((T_g, h)) if g is None else g["x"]
+    from paper_2601_08800_b200 import RouterSpec
+    router = RouterSpec.random(x.shape[0], E, k, seed=3) if g is None else _router(g)
+    E = router.num_experts
+    experts = ExpertSpec.default(E)
+    xt = torch.as_tensor(x).to(dtype).cuda()
+    y, _ = run_moe_block(build_cluster(n, m), xt, router, experts)
+    ids, w = router.arrays()
+    xr = xt.double().cpu().numpy()
+    y_ref = orc.dense_oracle(xr, ids, w, orc.affine_apply(experts.scales, experts.biases))
+    assert orc.verify_metric(y.double().cpu().numpy(), y_ref) <= tol
+
+
+# ----------------------------------------------------------------- router
+@pytest.mark.parametrize("T,E,k,renorm", [(64, 16, 4, True), (300, 128, 8, True),
+                                          (257, 256, 8, False), (128, 60, 6, True),
+                                          (1000, 1024, 8, True), (5, 8, 8, True)])
+def test_router_topk_bit_exact(T, E, k, renorm):
+    from paper_2601_08800_b200.plan import LayerPlan
+    rng = np.random.default_rng(T + E)
+    logits = rng.standard_normal((T, E)).astype(np.float32)
+    logits[0, :] = 0.5                       # all-equal row: ids 0..k-1
+    if T > 3:
+        logits[3, 1] = logits[3, E - 1] = 9.0  # exact tie -> lowest id first
+    ids_ref, w_ref = orc.router_topk(logits, k, renormalize=renorm)
+    plan = LayerPlan(1, 1, T, 8, E, k, dtype=torch.float32, renormalize=renorm)
+    plan.route(logits=torch.as_tensor(logits).cuda())
+    plan.layout(check_capacity=True)
+    v = plan.rank_views(0)
+    assert np.array_equal(v["ids"].cpu().numpy(), ids_ref)
+    np.testing.assert_allclose(v["weights"].cpu().numpy(), w_ref, rtol=2e-6, atol=1e-7)
+    counts = np.bincount(ids_ref.reshape(-1), minlength=E)
+    assert np.array_equal(v["cnt_all"].cpu().numpy()[0], counts)
+    assert np.array_equal(v["exp_cnt"].cpu().numpy(), counts)
+    plan.close()
+
+
+def test_router_topk_feeds_layer_2x2():
+    """Gate -> table on a 2x2 cluster equals the reference fed by our gate."""
+    from paper_2601_08800_b200 import build_routing_table
+    z = np.load(__import__("conftest").GOLDEN / "router_topk_logits.npz")
+    g = load_golden("ref_router_topk")
+    tab = build_routing_table(_router(g), 2, 32)
+    for d in range(2):
+        assert np.array_equal(tab.token[d], g[f"tok_{d}"])
+        assert np.array_equal(tab.expert[d], g[f"exp_{d}"])
+    assert np.array_equal(g["ids"], z["ids"].astype(np.int64))
+
+
+# ----------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("G,N,K,out", [(4, 256, 128, "bf16"), (3, 128, 192, "f32"),
+                                       (8, 512, 2048, "bf16"), (5, 768, 384, "f32")])
+def test_grouped_gemm_vs_torch_fp32(G, N, K, out):
+    from paper_2601_08800_b200 import _native
+    gen = torch.Generator(device="cuda").manual_seed(G * N + K)
+    cnts = torch.tensor([0, 1, 127, 128, 129, 300, 5, 256][:G], dtype=torch.int32)
+    offs = torch.zeros(G, dtype=torch.int32)
+    offs[1:] = torch.cumsum(cnts, 0)[:-1]
+    M = int(cnts.sum())
+    A = torch.randn(M + 64, K, device="cuda", generator=gen).to(torch.bfloat16)
+    B = (torch.randn(G, N, K, device="cuda", generator=gen) / K ** 0.5).to(torch.bfloat16)
+    dt = torch.bfloat16 if out == "bf16" else torch.float32
+    D = torch.full((M + 64, N), 7.0, device="cuda", dtype=dt)
+    _native.call("mx_grouped_gemm", A.data_ptr(), B.data_ptr(), D.data_ptr(),
+                 _native.MX_BF16 if out == "bf16" else _native.MX_F32,
+                 offs.cuda().data_ptr(), cnts.cuda().data_ptr(), G, M, N, K, 0,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for g in range(G):
+        o, c = int(offs[g]), int(cnts[g])
+        ref = A[o:o + c].float() @ B[g].float().T
+        got = D[o:o + c].float()
+        tol = 2e-2 if out == "bf16" else 1e-3
+        assert torch.allclose(got, ref, rtol=tol, atol=tol), (g, (got - ref).abs().max())
+    assert torch.all(D[M:].float() == 7.0)   # rows past the groups untouched
+
+
+def test_grouped_gemm_swiglu_epilogue():
+    from paper_2601_08800_b200 import _native
+    G, I, K = 3, 256, 256
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    cnts = torch.tensor([130, 0, 64], dtype=torch.int32)
+    offs = torch.tensor([0, 130, 130], dtype=torch.int32)
+    M = 194
+    A = torch.randn(M, K, device="cuda", generator=gen).to(torch.bfloat16)
+    wg = (torch.randn(G, I, K, device="cuda", generator=gen) / 16).to(torch.bfloat16)
+    wu = (torch.randn(G, I, K, device="cuda", generator=gen) / 16).to(torch.bfloat16)
+    w13 = torch.empty(G, 2 * I, K, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.current_stream().cuda_stream
+    _native.call("mx_swiglu_pack_w13", wg.data_ptr(), wu.data_ptr(), w13.data_ptr(), G, I, K, s)
+    D = torch.zeros(M, I, device="cuda", dtype=torch.bfloat16)
+    _native.call("mx_grouped_gemm", A.data_ptr(), w13.data_ptr(), D.data_ptr(), _native.MX_BF16,
+                 offs.cuda().data_ptr(), cnts.cuda().data_ptr(), G, M, 2 * I, K, 1, s)
+    torch.cuda.synchronize()
+    for g in range(G):
+        o, c = int(offs[g]), int(cnts[g])
+        gate = A[o:o + c].float() @ wg[g].float().T
+        up = A[o:o + c].float() @ wu[g].float().T
+        ref = torch.nn.functional.silu(gate) * up
+        assert torch.allclose(D[o:o + c].float(), ref, rtol=2e-2, atol=2e-2)
+
+
+# ----------------------------------------------------------------- SwiGLU layer
+@pytest.mark.parametrize("shape", [(1, 1), (2, 2), (4, 2), (2, 4), (1, 2)])
+def test_swiglu_layer_vs_oracle(shape):
+    from paper_2601_08800_b200 import (RouterSpec, SwiGLUExperts, build_cluster,
+                                       moe_oracle, run_moe_block)
+    n, m = shape
+    E, h, I, T_g, k = 16, 256, 512, 96 * n, 4
+    ex = SwiGLUExperts.random(E, h, I, seed=n * 10 + m)
+    x = torch.randn(T_g, h, device="cuda").to(torch.bfloat16)
+    router = RouterSpec.random(T_g, E, k, seed=5)
+    y, _ = run_moe_block(build_cluster(n, m), x, router, ex)
+    oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    ids, w = router.arrays()
+    y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
+    assert orc.verify_metric(y.float().cpu().numpy(), y_o) <= 2e-2
+    # the package's own dense GPU oracle agrees with the CPU one
+    y_d = moe_oracle(x, router, ex)
+    assert orc.verify_metric(y_d.double().cpu().numpy(), y_o) <= 1e-3

@@ -1,0 +1,92 @@
+"""Pin the CPU oracle to the reference's frozen outputs (CPU only)."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_names, load_golden
+from oracle import mixserve_oracle as orc
+
+
+def _meta(g):
+    return json.loads(str(g["meta"]))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_table_and_layout_bit_exact(name):
+    g = load_golden(name)
+    mt = _meta(g)
+    n, T = mt["n"], mt["tokens"] // mt["n"]
+    tab = orc.Table(g["ids"], g["weights"], n, T, mt["E"])
+    for d in range(n):
+        assert np.array_equal(tab.token[d], g[f"tok_{d}"])
+        assert np.array_equal(tab.expert[d], g[f"exp_{d}"])
+        assert np.array_equal(tab.src[d], g[f"src_{d}"])
+        assert np.array_equal(tab.weight[d], g[f"w_{d}"])
+        assert np.array_equal(tab.expert_major(d), g[f"emajor_{d}"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_fused_values_bit_exact(name):
+    g = load_golden(name)
+    mt = _meta(g)
+    E = mt["E"]
+    scales = [float(e + 1) for e in range(E)]
+    biases = [float(e) for e in range(E)]
+    y, _ = orc.run_fused_affine(mt["n"], mt["m"], g["x"], g["ids"],
+                                g["weights"], E, scales, biases)
+    # same association order as sim:433-441 / sim:506-520 -> identical f64
+    assert np.array_equal(y, g["y_fused"])
+    y_o = orc.dense_oracle(g["x"], g["ids"], g["weights"],
+                           orc.affine_apply(scales, biases))
+    assert np.array_equal(y_o, g["y_oracle"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_trace_bit_exact(name):
+    g = load_golden(name)
+    mt = _meta(g)
+    n, m, h = mt["n"], mt["m"], mt["h"]
+    T = mt["tokens"] // n
+    tab = orc.Table(g["ids"], g["weights"], n, T, mt["E"])
+    ev = orc.fused_trace(n, m, T, h, tab.send_counts(),
+                         [tab.expert_rows(d) for d in range(n)])
+    assert orc.trace_csv(ev) == str(g["trace_csv"])
+
+
+def test_reference_trace_2x2_bytes():
+    g = load_golden("ref_2x2_golden")
+    tab = orc.Table(g["ids"], g["weights"], 2, 2, 2)
+    ev = orc.fused_trace(2, 2, 2, 8, tab.send_counts(),
+                         [tab.expert_rows(d) for d in range(2)])
+    assert orc.trace_csv(ev).encode() == (GOLDEN / "trace_2x2.csv").read_bytes()
+    # SURVEY §8(c) worked case: y = [x0, 2*x1+1, x2, 2*x3+1]
+    x = g["x"]
+    assert np.array_equal(g["y_fused"],
+                          np.stack([x[0], 2 * x[1] + 1, x[2], 2 * x[3] + 1]))
+
+
+def test_swiglu_restatement_matches_reference_oracle():
+    g = load_golden("ref_swiglu")
+    ex = orc.SwiGLUOracle(g["wg"], g["wu"], g["wd"])
+    y = orc.moe_layer_swiglu(g["x"], g["ids"], g["weights"], ex)
+    assert orc.verify_metric(y, g["y_oracle"]) < 1e-6  # fp32 BLAS order
+    assert orc.verify_metric(g["y_baseline"], g["y_oracle"]) < 1e-12
+
+
+def test_router_topk_restatement_frozen():
+    z = np.load(GOLDEN / "router_topk_logits.npz")
+    ids, w = orc.router_topk(z["logits"], 4)
+    assert np.array_equal(ids, z["ids"])
+    assert np.array_equal(w, z["weights"])
+    # exact tie at row 3 between experts 5 and 9: lowest id first
+    assert list(ids[3, :2]) == [5, 9]
+    g = load_golden("ref_router_topk")
+    assert np.array_equal(g["ids"], ids.astype(np.int64))
+
+
+def test_bf16_round():
+    a = np.array([1.0, 1.00390625, 1.01171875, -3.14159], dtype=np.float32)
+    r = orc.bf16_round(a)
+    assert r[0] == 1.0 and r[1] == 1.0 and r[2] == 1.015625
+    assert abs(r[3] + 3.140625) < 1e-7
