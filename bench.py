@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""MoE-layer tokens/s of the B200 TP-EP layer (BASELINE.json metric).
+
+Workload: BASELINE.json configs[1], the Qwen3-30B-A3B-shaped MoE layer
+(h=2048, moe_intermediate=768, 128 experts, top-8, bf16 SwiGLU experts,
+fp32 gate logits) on a prefill batch of 8192 tokens; one step = one full
+layer forward (gate top-k -> dispatch -> grouped GEMM -> combine) over the
+8192 tokens.  Total work is fixed as N grows ("scaling": "strong"); the
+cluster is TP2 x EP(N/2) (config B's TP2xEP4 at N=8), pure 1x1 at N=1.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: CUDA events on the launching stream around every step, L2 flushed
+(256 MiB write) between steps outside the events, max over ranks.  Per-
+phase events inside the same timed steps give the roofline of the dominant
+kernel.  ``e2e`` repeats the step through the public API with pinned host
+inputs and the output copied back.  The CPU baseline is the oracle port
+(oracle/, numpy + BLAS, all host threads) on a bounded token sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+H, INTER, E, K_TOP, T_GLOBAL = 2048, 768, 128, 8, 8192
+NVLINK_PEER_GBS = 770.0      # measured peer copy, B200_PROFILING.md
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU
+def cpu_oracle_step(x, logits, experts_np):
+    """One bounded sample of the layer on the host: oracle gate + table +
+    batched SwiGLU experts (numpy/BLAS), expert-ascending accumulation."""
+    from oracle import mixserve_oracle as orc
+    ids, w = orc.router_topk(logits, K_TOP, renormalize=True)
+    return orc.moe_layer_swiglu(x, ids, w, experts_np)
+
+
+def cpu_baseline(sample_tokens=512, reps=3, seed=0):
+    import torch
+    from paper_2601_08800_b200 import SwiGLUExperts
+    from oracle import mixserve_oracle as orc
+    ex = SwiGLUExperts.random(E, H, INTER, seed=seed, device="cpu") \
+        if not torch.cuda.is_available() else SwiGLUExperts.random(E, H, INTER, seed=seed)
+    onp = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    rng = np.random.default_rng(seed)
+    x = orc.bf16_round(rng.standard_normal((sample_tokens, H)).astype(np.float32))
+    logits = rng.standard_normal((sample_tokens, E)).astype(np.float32)
+    cpu_oracle_step(x[:64], logits[:64], onp)   # warm BLAS
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        cpu_oracle_step(x, logits, onp)
+    dt = (time.perf_counter() - t0) / reps
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{sample_tokens} tokens of the {T_GLOBAL}-token Qwen3-shape batch "
+                      f"(oracle gate + SwiGLU experts, f32 numpy/BLAS), best of {reps}",
+            "seconds_per_sample": dt}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (oracle
+    port: the reference is pure Python and cannot travel to the GPU box),
+    rank 0 only, all host threads, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from paper_2601_08800_b200 import SwiGLUExperts
+    from oracle import mixserve_oracle as orc
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    ex = SwiGLUExperts.random(E, H, INTER, seed=0, device=dev)
+    onp = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    del ex
+    sample = args.ref_sample
+    rng = np.random.default_rng(1)
+    x = orc.bf16_round(rng.standard_normal((sample, H)).astype(np.float32))
+    logits = rng.standard_normal((sample, E)).astype(np.float32)
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_oracle_step(x, logits, onp)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_oracle_step(x, logits, onp)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    value = sample / dt
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": "MoE-layer tokens/s", "value": value,
+        "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "Qwen3-30B-A3B-shaped MoE layer, 8192-token prefill "
+                               f"(bounded sample of {sample} tokens per step)",
+                   "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{sample} tokens per step, oracle port (numpy/BLAS)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def phase_model(S, cnt, n, m, group, tp, T):
+    """Algorithmic bytes / flops per launch of every phase on this rank
+    (SURVEY.md §8(d)); S[j][d] = slots of group j hosted on group d."""
+    It = INTER // m
+    S_d = int(S[:, group].sum())             # rows this rank's GEMMs process
+    remote_in = int(S[:, group].sum() - S[group, group])   # rows received over NVLink
+    local_rows = int(S[group, group])
+    hb = H * 2
+    slots = T * K_TOP
+    model = {}
+    model["route"] = {"bound": "hbm", "bytes": T * E * 4 + slots * 16 + E * 4}
+    if n * m == 1:
+        model["dispatch"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
+        model["combine"] = {"bound": "hbm", "bytes": slots * hb + T * hb}
+    else:
+        model["dispatch"] = {"bound": "nvlink", "bytes": remote_in * hb,
+                             "local_hbm_bytes": 2 * local_rows * hb}
+        # pulls: every slot's column shard from the m TP ranks of its host,
+        # minus the one local read; plus the (m-1)/m of y pushed by TP peers
+        own_host_slots = int(S[group, group])
+        remote_pull = (slots * m - own_host_slots) * (H // m) * 2
+        model["combine"] = {"bound": "nvlink",
+                            "bytes": remote_pull + T * H * (m - 1) // m * 2}
+    model["gemm1_swiglu"] = {"bound": "tensor", "flops": 2 * S_d * H * 2 * It}
+    model["gemm2"] = {"bound": "tensor", "flops": 2 * S_d * It * H}
+    return model
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2601_08800_b200 import SwiGLUExperts
+    from paper_2601_08800_b200.layer import MoELayer, layout_for
+
+    n, m = layout_for(world, args.tp)
+    group, tp = divmod(rank, m)
+    T = T_GLOBAL // n
+    ex = SwiGLUExperts.random(E, H, INTER, seed=0)
+    w13, w2 = ex.rank_shard(n, m, rank)
+    del ex
+    torch.cuda.empty_cache()
+    layer = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank)
+    g = torch.Generator(device="cuda").manual_seed(1000 + group)
+    x = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    logits = torch.randn(T, E, device="cuda", generator=g)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        layer.forward(x, logits)
+    sync_all()
+    S = layer.routing_counts()[1].astype(np.int64)
+    cnt = layer.routing_counts()[0]
+
+    # ---- timed region: K steps, per-phase events, L2 flushed in between
+    per_step, phase_times = [], {}
+    with ClockSampler(local) as clk:
+        sync_all()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            evs = []
+            layer.forward_phases(x, logits, evs, stream=stream)
+            per_step.append(evs)
+        torch.cuda.synchronize()
+    step_ms = []
+    for evs in per_step:
+        step_ms.append(evs[0][1].elapsed_time(evs[-1][1]))
+        for (a, ea), (b, eb) in zip(evs[:-1], evs[1:]):
+            phase_times.setdefault(b, []).append(ea.elapsed_time(eb))
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = T_GLOBAL / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API: pinned host in, host out
+    x_h = x.cpu().pin_memory()
+    l_h = logits.cpu().pin_memory()
+    y_h = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+    copy_out = tp == 0
+    for _ in range(2):
+        layer.forward(x_h, l_h, out=y_h if copy_out else None)
+    sync_all()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        layer.forward(x_h, l_h, out=y_h if copy_out else None)
+        b.record(stream)
+        e2e_ms.append((a, b))
+    torch.cuda.synchronize()
+    e2e_total = sum(a.elapsed_time(b) for a, b in e2e_ms)
+    t = torch.tensor([e2e_total], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_step = float(t.item()) / args.steps
+    h2d = (x_h.numel() * 2 + l_h.numel() * 4) * world
+    d2h = y_h.numel() * 2 * n
+
+    # ---- NCCL AR + A2A baseline on the same config (N > 1)
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        for _ in range(2):
+            layer.forward_baseline(x, logits)
+        sync_all()
+        bl = []
+        for _ in range(max(3, args.steps // 2)):
+            flush.fill_(1)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            layer.forward_baseline(x, logits)
+            b.record(stream)
+            bl.append((a, b))
+        torch.cuda.synchronize()
+        blt = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in bl]))], device="cuda")
+        dist.all_reduce(blt, op=dist.ReduceOp.MAX)
+        nccl = {"ms_per_step": float(blt.item()),
+                "tokens_per_s": T_GLOBAL / (float(blt.item()) / 1e3),
+                "layout": "NCCL all_to_all_single x2 (full width, every TP rank) + TP all_reduce",
+                "fused_speedup": float(blt.item()) / ms_per_step}
+
+    # ---- roofline of the dominant kernel (this rank; rank 0 reports)
+    pk, pk_kind = peaks()
+    model = phase_model(S, cnt, n, m, group, tp, T)
+    avg = {k: float(np.mean(v)) for k, v in phase_times.items()}
+    rooflines = {}
+    for ph, spec in model.items():
+        if ph not in avg or avg[ph] <= 0:
+            continue
+        sec = avg[ph] / 1e3
+        if spec["bound"] == "tensor":
+            ach = spec["flops"] / sec / 1e12
+            peak, unit = pk["bf16_tflops_sustained"], "TFLOP/s"
+            peak_src = f"{pk_kind} bf16 sustained"
+        elif spec["bound"] == "hbm":
+            ach = spec["bytes"] / sec / 1e9
+            peak, unit = pk["hbm_gbs"], "GB/s"
+            peak_src = f"{pk_kind} HBM copy"
+        else:
+            ach = spec["bytes"] / sec / 1e9
+            peak, unit = NVLINK_PEER_GBS, "GB/s"
+            peak_src = "NVLink peer copy 770 GB/s/direction (B200_PROFILING.md)"
+        rooflines[ph] = {"bound": spec["bound"], "achieved": ach, "peak": peak, "unit": unit,
+                         "frac": ach / peak, "us": avg[ph] * 1e3, "peak_source": peak_src}
+    kernels = {k: v for k, v in rooflines.items()}
+    dom = max(kernels, key=lambda k: kernels[k]["us"]) if kernels else None
+    traffic = None
+    tp_file = ROOT / "profiles" / "traffic.json"
+    if dom and tp_file.exists():
+        traffic = json.loads(tp_file.read_text()).get(f"n{world}", {}).get(dom)
+    roof = dict(kernels[dom]) if dom else None
+    if roof is not None:
+        roof["kernel"] = dom
+        roof["traffic"] = traffic
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(sample_tokens=args.cpu_sample)
+
+    launches_per_step = 7 + (4 if world > 1 else 0)
+    if rank == 0:
+        line = {
+            "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "Qwen3-30B-A3B-shaped MoE layer (BASELINE configs[1]), "
+                                   "8192-token prefill, bf16 SwiGLU experts, fp32 gate logits",
+                       "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP,
+                       "global_tokens": T_GLOBAL, "groups_n": n, "tp_m": m,
+                       "parallelism": f"TP{m}xEP{n}", "l2": "flushed (256 MiB write) between steps",
+                       "weights": "random init, seed 0"},
+            "clocks": clk.summary(),
+            "e2e": {"value": T_GLOBAL / (e2e_step / 1e3), "unit": "tokens/s",
+                    "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "note": "public MoELayer.forward with pinned host x/logits in and y out"},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof,
+            "rooflines": rooflines,
+            "phases_us": {k: v * 1e3 for k, v in avg.items()},
+            "cpu_baseline": cpu,
+        }
+        if nccl is not None:
+            line["nccl_baseline"] = nccl
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tp", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=512)
+    ap.add_argument("--ref-sample", type=int, default=512)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -147,6 +147,10 @@ MX_API int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream);
 /* K3 expert compute on this rank's received rows -> TP partials
  * (affine stand-in sim:535-562, or the SwiGLU grouped GEMM).             */
 MX_API int mx_expert(mx_plan* p, int rank, const mx_expert_params* ep, void* stream);
+/* The same expert compute split in its launches, for per-kernel timing:
+ * stage 1 = GEMM1 + SwiGLU epilogue, stage 2 = GEMM2, 0 = both.          */
+MX_API int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
+                           void* stream);
 /* K4 fused RS-combine (sim:410-521): the owner pulls its column shard of
  * every slot's TP partials (rank-ascending sum = the intra reduce-scatter),
  * weights and accumulates in the reference's host arrival order, and

@@ -68,6 +68,7 @@ SIGNATURES = {
     "mx_layout": [VP, I, I, VP],
     "mx_dispatch": [VP, I, VP, VP],
     "mx_expert": [VP, I, C.POINTER(ExpertParams), VP],
+    "mx_expert_stage": [VP, I, C.POINTER(ExpertParams), I, VP],
     "mx_combine": [VP, I, VP, VP],
     "mx_forward": [VP, I, VP, VP, VP, VP, C.POINTER(ExpertParams), VP, VP],
     "mx_baseline_dispatch_pack": [VP, I, VP, VP, VP, VP],

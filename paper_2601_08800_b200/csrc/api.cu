@@ -32,7 +32,17 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 // scope), then wait until every peer has published it into ours (acquire).
 // One thread per peer.  A watchdog turns a lost peer into an error flag
 // instead of a hang (SURVEY.md §5 failure detection).
-__global__ void k_barrier(DevView v, unsigned long long epoch) {
+__global__ void k_barrier(DevView v) {
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) {
+    // epochs live on the device so the barrier can be replayed in a CUDA graph;
+    // every rank runs the same barrier sequence, so the counters agree
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
+        at<int>(v, v.rank, v.off.counters) + 2);
+    s_epoch = ++(*ctr);
+  }
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
   const int r = threadIdx.x;
   if (r < v.W) {
     __threadfence_system();
@@ -50,8 +60,8 @@ __global__ void k_barrier(DevView v, unsigned long long epoch) {
   __threadfence_system();
 }
 
-int launch_barrier(const DevView& v, unsigned long long epoch, cudaStream_t s) {
-  k_barrier<<<1, 64, 0, s>>>(v, epoch);
+int launch_barrier(const DevView& v, cudaStream_t s) {
+  k_barrier<<<1, 64, 0, s>>>(v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -312,7 +322,7 @@ int mx_comm_barrier(mx_comm* c, void* stream) {
   DevView v{};
   v.rank = c->rank; v.W = c->W; v.off = c->off;
   for (int r = 0; r < c->W; ++r) v.heap[r] = c->heap[r];
-  return launch_barrier(v, ++c->epoch, static_cast<cudaStream_t>(stream));
+  return launch_barrier(v, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
@@ -347,7 +357,7 @@ int barrier(mx_plan* p, cudaStream_t s) {
   mx_comm* c = p->comm;
   if (c->emulate || c->W == 1) return MX_OK;
   DevView v = view_for(p, c->rank);
-  return launch_barrier(v, ++c->epoch, s);
+  return launch_barrier(v, s);
 }
 
 int check_errors(mx_plan* p, int first, int last) {
@@ -425,29 +435,33 @@ int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream) {
   return MX_OK;
 }
 
-int mx_expert(mx_plan* p, int rank, const mx_expert_params* ep, void* stream) {
+int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage, void* stream) {
   RankIter it;
   int rc = ranks_for(p, rank, &it);
   if (rc) return rc;
+  if (stage < 0 || stage > 2) { set_error("stage must be 0, 1 or 2"); return MX_ERR_INVALID; }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
     if (p->d.expert_kind == MX_EXPERT_AFFINE) {
+      if (stage == 2) continue;  // single-kernel expert
       rc = launch_expert_affine(v, ep->scales, ep->biases, s);
     } else {
       // emulated: per-rank weight shards stacked rank-major
-      const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
       const int Elmax = (v.E + v.n - 1) / v.n;
-      (void)El;
       const size_t w13_rank = (size_t)Elmax * 2 * v.I_t * v.h * 2;
       const size_t w2_rank = (size_t)Elmax * v.h * v.I_t * 2;
       const int slot = p->comm->emulate ? r : 0;
       rc = launch_expert_swiglu(v, static_cast<const char*>(ep->w13) + slot * w13_rank,
-                                static_cast<const char*>(ep->w2) + slot * w2_rank, s);
+                                static_cast<const char*>(ep->w2) + slot * w2_rank, stage, s);
     }
     if (rc) return rc;
   }
   return MX_OK;
+}
+
+int mx_expert(mx_plan* p, int rank, const mx_expert_params* ep, void* stream) {
+  return mx_expert_stage(p, rank, ep, 0, stream);
 }
 
 int mx_combine(mx_plan* p, int rank, void* y_out, void* stream) {

@@ -33,7 +33,7 @@ __device__ __forceinline__ int block_pos(const DevView& v, const int* s_pre, int
   const size_t si = (size_t)t * v.k + i;
   const int e = at<int>(v, v.rank, v.off.ids)[si];
   const int c = t / MX_CHUNK;
-  return s_pre[e] + at<int>(v, v.rank, v.off.chunk_hist)[c * v.E + e] +
+  return s_pre[e] + at<int>(v, v.rank, v.off.chunk_hist)[e * v.C + c] +
          at<int>(v, v.rank, v.off.slot_rank)[si];
 }
 

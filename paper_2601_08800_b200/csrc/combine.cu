@@ -17,8 +17,10 @@
 
 namespace mx {
 
-template <int DT, bool VEC>
-__global__ void __launch_bounds__(256) k_combine(DevView v) {
+// KU > 0: unrolled fast path for k <= KU -- every slot's load of a column
+// vector is issued before any is consumed (KU x 16 B in flight per lane).
+template <int DT, bool VEC, int KU>
+__global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = VEC ? Elt<DT>::V : 1;  // elements per 16 B vector
@@ -58,44 +60,107 @@ __global__ void __launch_bounds__(256) k_combine(DevView v) {
       s_w[warp][rk] = w;
     }
     __syncwarp();
-    for (int c = c0 + lane * V; c < c1; c += 32 * V) {
-      A acc[V];
+    if constexpr (KU > 0) {
+      // exact mode (f64) keeps the reference association: per slot the TP
+      // partials are summed rank-ascending first, then weighted (sim:436-441,
+      // sim:519); the fp32-accumulating modes fold w into each partial,
+      // which halves the live registers.
+      constexpr bool EXACT = DT == MX_F64;
+      A ws[KU];
 #pragma unroll
-      for (int q = 0; q < V; ++q) acc[q] = (A)0;
-      for (int s = 0; s < k; ++s) {
-        const size_t off = (size_t)s_pos[warp][s] * h + c;
-        const int r0 = s_src[warp][s];
-        A red[V];
-        if constexpr (VEC) {
-          uint4 raw = ld_v4(at<T>(v, r0, v.off.partial) + off);
-          const T* pv = reinterpret_cast<const T*>(&raw);
+      for (int s = 0; s < KU; ++s) ws[s] = s_w[warp][s < k ? s : 0];
+      for (int c = c0 + lane * V; c < c1; c += 32 * V) {
+        A red[EXACT ? KU : 1][V];
+        A acc[V];
 #pragma unroll
-          for (int q = 0; q < V; ++q) red[q] = to_acc(pv[q]);
-          for (int tt = 1; tt < m; ++tt) {
-            uint4 r2 = ld_v4(at<T>(v, r0 + tt, v.off.partial) + off);
-            const T* p2 = reinterpret_cast<const T*>(&r2);
+        for (int q = 0; q < V; ++q) acc[q] = (A)0;
 #pragma unroll
-            for (int q = 0; q < V; ++q) red[q] = add_rn(red[q], to_acc(p2[q]));
+        for (int tt = 0; tt < 8; ++tt) {
+          if (tt >= m) break;
+          uint4 raw[KU];
+#pragma unroll
+          for (int s = 0; s < KU; ++s) {
+            if (s < k) {
+              const int r = s_src[warp][s] + tt;
+              const T* p = at<T>(v, r, v.off.partial) + (size_t)s_pos[warp][s] * h + c;
+              if constexpr (VEC) raw[s] = ld_v4(p);
+              else { T one = *p; raw[s].x = 0; *reinterpret_cast<T*>(&raw[s]) = one; }
+            }
           }
-        } else {
-          red[0] = to_acc(at<T>(v, r0, v.off.partial)[off]);
-          for (int tt = 1; tt < m; ++tt)
-            red[0] = add_rn(red[0], to_acc(at<T>(v, r0 + tt, v.off.partial)[off]));
+#pragma unroll
+          for (int s = 0; s < KU; ++s) {
+            if (s < k) {
+              const T* pv = reinterpret_cast<const T*>(&raw[s]);
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                if constexpr (EXACT)
+                  red[s][q] = tt == 0 ? to_acc(pv[q]) : add_rn(red[s][q], to_acc(pv[q]));
+                else
+                  acc[q] = fmaf(ws[s], to_acc(pv[q]), acc[q]);
+              }
+            }
+          }
         }
-        const A ws = s_w[warp][s];
+        if constexpr (EXACT) {
 #pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(ws, red[q]));
+          for (int s = 0; s < KU; ++s)
+            if (s < k) {
+#pragma unroll
+              for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(ws[s], red[s][q]));
+            }
+        }
+        // final intra-group all-gather: push the shard to every TP rank
+        for (int tt = 0; tt < m; ++tt) {
+          T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)tl * h + c;
+          if constexpr (VEC) {
+            T outv[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) outv[q] = from_acc<T>(acc[q]);
+            st_v4(y, *reinterpret_cast<uint4*>(outv));
+          } else {
+            y[0] = from_acc<T>(acc[0]);
+          }
+        }
       }
-      // final intra-group all-gather: push the shard to every TP rank
-      for (int tt = 0; tt < m; ++tt) {
-        T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)tl * h + c;
-        if constexpr (VEC) {
-          T outv[V];
+    } else {
+      for (int c = c0 + lane * V; c < c1; c += 32 * V) {
+        A acc[V];
 #pragma unroll
-          for (int q = 0; q < V; ++q) outv[q] = from_acc<T>(acc[q]);
-          st_v4(y, *reinterpret_cast<uint4*>(outv));
-        } else {
-          y[0] = from_acc<T>(acc[0]);
+        for (int q = 0; q < V; ++q) acc[q] = (A)0;
+        for (int s = 0; s < k; ++s) {
+          const size_t off = (size_t)s_pos[warp][s] * h + c;
+          const int r0 = s_src[warp][s];
+          A red[V];
+          if constexpr (VEC) {
+            uint4 raw = ld_v4(at<T>(v, r0, v.off.partial) + off);
+            const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+            for (int q = 0; q < V; ++q) red[q] = to_acc(pv[q]);
+            for (int tt = 1; tt < m; ++tt) {
+              uint4 r2 = ld_v4(at<T>(v, r0 + tt, v.off.partial) + off);
+              const T* p2 = reinterpret_cast<const T*>(&r2);
+#pragma unroll
+              for (int q = 0; q < V; ++q) red[q] = add_rn(red[q], to_acc(p2[q]));
+            }
+          } else {
+            red[0] = to_acc(at<T>(v, r0, v.off.partial)[off]);
+            for (int tt = 1; tt < m; ++tt)
+              red[0] = add_rn(red[0], to_acc(at<T>(v, r0 + tt, v.off.partial)[off]));
+          }
+          const A ws = s_w[warp][s];
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(ws, red[q]));
+        }
+        for (int tt = 0; tt < m; ++tt) {
+          T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)tl * h + c;
+          if constexpr (VEC) {
+            T outv[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) outv[q] = from_acc<T>(acc[q]);
+            st_v4(y, *reinterpret_cast<uint4*>(outv));
+          } else {
+            y[0] = from_acc<T>(acc[0]);
+          }
         }
       }
     }
@@ -109,8 +174,9 @@ static void launch_combine_dt(const DevView& v, int blocks, cudaStream_t s) {
   col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
   const bool vec = ((size_t)c0 * v.elt) % 16 == 0 && ((size_t)(c1 - c0) * v.elt) % 16 == 0 &&
                    ((size_t)v.h * v.elt) % 16 == 0;
-  if (vec) k_combine<DT, true><<<blocks, 256, 0, s>>>(v);
-  else k_combine<DT, false><<<blocks, 256, 0, s>>>(v);
+  if (vec && v.k <= 8 && v.m <= 8) k_combine<DT, true, 8><<<blocks, 256, 0, s>>>(v);
+  else if (vec) k_combine<DT, true, 0><<<blocks, 256, 0, s>>>(v);
+  else k_combine<DT, false, 0><<<blocks, 256, 0, s>>>(v);
 }
 
 int launch_combine(const DevView& v, cudaStream_t s) {

@@ -432,15 +432,18 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
 }
 
 // Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.
-int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, cudaStream_t s) {
+int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
+                         cudaStream_t s) {
   const int e0 = first_expert(v.group, v.n, v.E), e1 = first_expert(v.group + 1, v.n, v.E);
   const int El = e1 - e0;
   if (El == 0) return MX_OK;
   const int32_t* offs = at<int32_t>(v, v.rank, v.off.exp_off) + e0;
   const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
-  int rc = grouped_gemm(at<char>(v, v.rank, v.off.recv), w13, at<char>(v, v.rank, v.off.act),
-                        MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, 2 * v.I_t, v.h, 1, s);
-  if (rc) return rc;
+  if (stage != 2) {
+    int rc = grouped_gemm(at<char>(v, v.rank, v.off.recv), w13, at<char>(v, v.rank, v.off.act),
+                          MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, 2 * v.I_t, v.h, 1, s);
+    if (rc || stage == 1) return rc;
+  }
   return grouped_gemm(at<char>(v, v.rank, v.off.act), w2, at<char>(v, v.rank, v.off.partial),
                       MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s);
 }

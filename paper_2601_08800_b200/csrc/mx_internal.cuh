@@ -54,7 +54,7 @@ struct Offsets {
   size_t send;        // int32 [n][n]
   size_t tm_off;      // int32 [n][n]
   size_t host_rows;   // int32 [n]
-  size_t counters;    // int32 [16]
+  size_t counters;    // int32 [16]  [0]=route CTA counter [2..3]=u64 barrier epoch
   size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
   size_t total;
 };
@@ -148,10 +148,10 @@ int launch_layout(const DevView& v, cudaStream_t s);
 int launch_dispatch(const DevView& v, const void* x, cudaStream_t s);
 int launch_expert_affine(const DevView& v, const void* scales, const void* biases,
                          cudaStream_t s);
-int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2,
+int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
                          cudaStream_t s);
 int launch_combine(const DevView& v, cudaStream_t s);
-int launch_barrier(const DevView& v, unsigned long long epoch, cudaStream_t s);
+int launch_barrier(const DevView& v, cudaStream_t s);
 int launch_baseline_dispatch_pack(const DevView& v, const void* x, void* send,
                                   int32_t* counts, cudaStream_t s);
 int launch_baseline_dispatch_unpack(const DevView& v, const void* recv, cudaStream_t s);

@@ -19,8 +19,8 @@
 namespace mx {
 
 // One CTA per chunk of MX_CHUNK tokens of this rank's group.
-template <class WT>
-__global__ void __launch_bounds__(256)
+template <class WT, int EV>
+__global__ void __launch_bounds__(512)
 k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__ ids_in,
         const WT* __restrict__ w_in) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -30,7 +30,6 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
   int* s_ids = reinterpret_cast<int*>(smem);                      // [CHUNK*k]
   unsigned* s_mask = reinterpret_cast<unsigned*>(s_ids + MX_CHUNK * k);  // [E][4]
   int* s_hc = reinterpret_cast<int*>(s_mask + E * 4);             // [CHUNK][n]
-  __shared__ int s_last;
 
   int* ids = at<int>(v, v.rank, v.off.ids);
   WT* w = at<WT>(v, v.rank, v.off.w);
@@ -39,7 +38,6 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
   int* chunk_hist = at<int>(v, v.rank, v.off.chunk_hist);
   int* chunk_host = at<int>(v, v.rank, v.off.chunk_host);
   int* err = at<int>(v, v.rank, v.off.err);
-  int* counters = at<int>(v, v.rank, v.off.counters);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 
   for (int i = threadIdx.x; i < E * 4; i += blockDim.x) s_mask[i] = 0;
@@ -51,9 +49,9 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     const bool vec = (E % 4) == 0;
     for (int tl = warp; tl < nt; tl += nw) {
       const float* row = logits + (size_t)(t0 + tl) * E;
-      float val[MX_EMAX / 32];
+      float val[EV * 4];
 #pragma unroll
-      for (int i = 0; i < MX_EMAX / 128; ++i) {
+      for (int i = 0; i < EV; ++i) {
         const int e0 = 128 * i + 4 * lane;
         if (vec && e0 < E) {
           float4 f = __ldg(reinterpret_cast<const float4*>(row + e0));
@@ -71,7 +69,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
         float bv = -INFINITY;
         int be = 0x7fffffff;
 #pragma unroll
-        for (int i = 0; i < MX_EMAX / 32; ++i) {
+        for (int i = 0; i < EV * 4; ++i) {
           const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
           const bool ok = e < E && !((taken >> i) & 1u);
           if (ok && (val[i] > bv || (val[i] == bv && e < be))) { bv = val[i]; be = e; }
@@ -95,7 +93,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
       } else {
         float s = 0.f;
 #pragma unroll
-        for (int i = 0; i < MX_EMAX / 32; ++i) {
+        for (int i = 0; i < EV * 4; ++i) {
           const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
           if (e < E) s += expf(val[i] - mx);
         }
@@ -174,7 +172,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
       if (tl < MX_CHUNK) s_hc[tl * n + d] = ex;
       ex += a[q];
     }
-    if (lane == 31) chunk_host[c * n + d] = incl;
+    if (lane == 31) chunk_host[d * v.C + c] = incl;
   }
   __syncthreads();
   if (threadIdx.x < nt) {
@@ -186,38 +184,43 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     }
   }
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    chunk_hist[c * E + e] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
-                            __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
+    chunk_hist[e * v.C + c] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
+                              __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
   }
-
-  // ---- last CTA: exclusive chunk prefix per expert / host, totals, publish
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(counters, 1) == (int)gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int C = gridDim.x;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int cc = 0; cc < C; ++cc) {
-      const int hv = __ldcg(chunk_hist + cc * E + e);
-      chunk_hist[cc * E + e] = run;
-      run += hv;
-    }
-    // publish this group's count row to every rank (peer stores in SPMD)
-    for (int r = 0; r < v.W; ++r) at<int>(v, r, v.off.cnt_all)[v.group * E + e] = run;
-  }
-  for (int d = threadIdx.x; d < n; d += blockDim.x) {
-    int run = 0;
-    for (int cc = 0; cc < C; ++cc) {
-      const int hv = __ldcg(chunk_host + cc * n + d);
-      chunk_host[cc * n + d] = run;
-      run += hv;
-    }
-  }
-  if (threadIdx.x == 0) counters[0] = 0;
 }
+
+// Exclusive prefix of the chunk counts, one warp per expert (and per host),
+// coalesced over the expert-major [E][C] layout; publishes the group's
+// per-expert totals into every rank's count matrix (peer stores in SPMD).
+__global__ void __launch_bounds__(256) k_route_scan(DevView v) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int E = v.E, n = v.n, C = v.C;
+  int* row;
+  if (w < E) row = at<int>(v, v.rank, v.off.chunk_hist) + (size_t)w * C;
+  else if (w < E + n) row = at<int>(v, v.rank, v.off.chunk_host) + (size_t)(w - E) * C;
+  else return;
+  int carry = 0;
+  for (int base = 0; base < C; base += 32) {
+    const int c = base + lane;
+    const int x = (c < C) ? row[c] : 0;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (c < C) row[c] = carry + incl - x;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (w < E && lane < v.W) {
+    at<int>(v, lane, v.off.cnt_all)[v.group * E + w] = carry;
+  }
+  if (w < E && v.W > 32) {
+    for (int r = 32 + lane; r < v.W; r += 32) at<int>(v, r, v.off.cnt_all)[v.group * E + w] = carry;
+  }
+}
+
 
 // Offsets of the layout from the gathered [n][E] count matrix (one CTA).
 __global__ void __launch_bounds__(1024) k_layout_meta(DevView v) {
@@ -302,34 +305,47 @@ __global__ void k_slotpos(DevView v) {
     const int d = home_of(e, n, E);
     const int c = t / MX_CHUNK;
     const long long pos = (long long)exp_off[e] + grp_off[v.group * E + e] +
-                          chunk_hist[c * E + e] + slot_rank[s];
-    const int tm = tm_off[v.group * n + d] + chunk_host[c * n + d] + slot_tmr[s];
+                          chunk_hist[e * v.C + c] + slot_rank[s];
+    const int tm = tm_off[v.group * n + d] + chunk_host[d * v.C + c] + slot_tmr[s];
     if (pos >= v.cap) atomicOr(err + 3, 1);
     slot_pos[s] = (int)pos;
     slot_tm[s] = tm;
   }
 }
 
+template <class WT, int EV>
+static int launch_route_ev(const DevView& v, int C, size_t smem, const float* logits,
+                           const int32_t* ids, const void* w, cudaStream_t s) {
+  auto kern = k_route<WT, EV>;
+  static bool attr = false;
+  if (!attr) {
+    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  kern<<<C, 512, smem, s>>>(v, logits, ids, static_cast<const WT*>(w));
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+template <class WT>
+static int launch_route_wt(const DevView& v, int C, size_t smem, const float* logits,
+                           const int32_t* ids, const void* w, cudaStream_t s) {
+  if (v.E <= 128) return launch_route_ev<WT, 1>(v, C, smem, logits, ids, w, s);
+  if (v.E <= 256) return launch_route_ev<WT, 2>(v, C, smem, logits, ids, w, s);
+  if (v.E <= 512) return launch_route_ev<WT, 4>(v, C, smem, logits, ids, w, s);
+  return launch_route_ev<WT, 8>(v, C, smem, logits, ids, w, s);
+}
+
 int launch_route(const DevView& v, const float* logits, const int32_t* ids,
                  const void* w, cudaStream_t s) {
-  const int C = (v.T + MX_CHUNK - 1) / MX_CHUNK;
+  const int C = v.C;
   if (C == 0) return MX_OK;
   const size_t smem = (size_t)MX_CHUNK * v.k * 4 + (size_t)v.E * 16 + (size_t)MX_CHUNK * v.n * 4;
-  if (v.elt == 8) {
-    static bool attr = false;
-    if (!attr) {
-      MX_CUDA(cudaFuncSetAttribute(k_route<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
-    k_route<double><<<C, 256, smem, s>>>(v, logits, ids, static_cast<const double*>(w));
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      MX_CUDA(cudaFuncSetAttribute(k_route<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
-    k_route<float><<<C, 256, smem, s>>>(v, logits, ids, static_cast<const float*>(w));
-  }
+  int rc = v.elt == 8 ? launch_route_wt<double>(v, C, smem, logits, ids, w, s)
+                      : launch_route_wt<float>(v, C, smem, logits, ids, w, s);
+  if (rc) return rc;
+  const int warps = v.E + v.n;
+  k_route_scan<<<(warps + 7) / 8, 256, 0, s>>>(v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }

@@ -1,0 +1,194 @@
+"""SPMD TP-EP MoE layer: one process per GPU, NVLink peer heaps.
+
+This is the serving-side entry of the same hot path as ``run_moe_block``
+(sim:565-595): rank ``r = group*m + tp`` (node-major, sim:63-67) owns the
+tokens of its group (replicated across the group's TP ranks, sim:383-384),
+the experts of its group (contiguous, sim:210-212) with the TP shard ``tp``
+of their intermediate dimension, and after ``forward`` the combined output
+of its group's tokens.
+
+``forward`` runs the fused path (K1 route -> K2 dispatch -> K3 grouped GEMM
+-> K4 combine, device flag barriers between phases).  ``forward_baseline``
+runs the NCCL AR + A2A layout of ``_run_baseline`` (sim:598-680) on the
+same buffers, for the fused-vs-NCCL comparison of BASELINE.json.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .plan import LayerPlan, stream_ptr
+from .simcluster import SwiGLUExperts
+
+
+def layout_for(world: int, tp: int | None = None):
+    """(n_group, tp) for a world size; default keeps TP=2 (config B,
+    TP2 x EP4 at 8 GPUs) and falls back to pure TP/EP for 1 GPU."""
+    if tp is None:
+        tp = 1 if world == 1 else 2
+    if world % tp:
+        raise ValueError(f"world {world} not divisible by tp {tp}")
+    return world // tp, tp
+
+
+class MoELayer:
+    def __init__(self, n, m, tokens_per_group, hidden, num_experts, top_k,
+                 inter, experts: SwiGLUExperts | None = None, *, rank=None,
+                 w13=None, w2=None, dtype=torch.bfloat16, renormalize=True,
+                 capacity=None, expert_kind="swiglu", scales=None, biases=None,
+                 process_group=None):
+        self.n, self.m, self.W = n, m, n * m
+        if rank is None:
+            rank = dist.get_rank() if dist.is_initialized() else 0
+        self.rank = rank
+        self.group, self.tp_rank = divmod(rank, m)
+        self.T, self.h, self.E, self.k, self.I = (tokens_per_group, hidden,
+                                                  num_experts, top_k, inter)
+        self.dtype = dtype
+        self.plan = LayerPlan(n, m, tokens_per_group, hidden, num_experts,
+                              top_k, dtype=dtype, expert_kind=expert_kind,
+                              inter=inter, renormalize=renormalize,
+                              capacity=capacity, emulate=False, rank=rank,
+                              process_group=process_group)
+        if expert_kind == "swiglu":
+            if w13 is None:
+                w13, w2 = experts.rank_shard(n, m, rank)
+            self.w13, self.w2 = w13, w2
+            self.params = N.ExpertParams(None, None, w13.data_ptr(), w2.data_ptr())
+        else:
+            acc = torch.float64 if dtype is torch.float64 else torch.float32
+            self.scales = torch.as_tensor(np.asarray(scales), device="cuda").to(acc)
+            self.biases = torch.as_tensor(np.asarray(biases), device="cuda").to(acc)
+            self.params = N.ExpertParams(self.scales.data_ptr(),
+                                         self.biases.data_ptr(), None, None)
+        self.y = self.plan.y_view(rank)
+        self._ep_group = self._tp_group = None
+
+    # ------------------------------------------------------------ fused path
+    def forward(self, x, logits=None, ids=None, weights=None, out=None,
+                stream=None):
+        """Fused layer forward.  ``x``: [T, h] tokens of this rank's group
+        (device, or pinned host -> copied in); ``logits`` [T, E] f32 or
+        ``ids``/``weights`` [T, k].  Returns the [T, h] output (a view of the
+        layer's buffer, valid until the next call, or ``out`` when given --
+        a host ``out`` receives a device-to-host copy)."""
+        dev = self.plan.device
+        if not x.is_cuda:
+            x = x.to(dev, non_blocking=True)
+        if logits is not None and not logits.is_cuda:
+            logits = logits.to(dev, non_blocking=True)
+        self.plan.forward(x, self.params, logits=logits, ids=ids,
+                          weights=weights, rank=self.rank, stream=stream)
+        if out is None:
+            return self.y
+        out.copy_(self.y, non_blocking=True)
+        return out
+
+    def forward_phases(self, x, logits, events, stream=None):
+        """Same launches as :meth:`forward`, phase by phase, recording a CUDA
+        event after each phase (for per-kernel timing in bench.py)."""
+        p, r = self.plan, self.rank
+        s = stream or torch.cuda.current_stream()
+        lib = N.load()
+        sp = stream_ptr(s)
+
+        def mark(name):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(s)
+            events.append((name, ev))
+
+        mark("start")
+        p.route(logits=logits, rank=r, stream=s); mark("route")
+        p.barrier(stream=s); mark("barrier_counts")
+        p.layout(rank=r, stream=s); mark("layout")
+        p.dispatch(x, rank=r, stream=s); mark("dispatch")
+        p.barrier(stream=s); mark("barrier_dispatch")
+        N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 1, sp), "gemm1")
+        mark("gemm1_swiglu")
+        N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 2, sp), "gemm2")
+        mark("gemm2")
+        p.barrier(stream=s); mark("barrier_partials")
+        p.combine(rank=r, stream=s); mark("combine")
+        p.barrier(stream=s); mark("barrier_out")
+        return self.y
+
+    def routing_counts(self):
+        """(cnt_all [n,E], send [n,n]) of the last forward, on the host."""
+        v = self.plan.rank_views(self.rank)
+        return v["cnt_all"].cpu().numpy(), v["send"].cpu().numpy()
+
+    # ------------------------------------------------------------ NCCL baseline
+    def _groups(self):
+        if self._ep_group is None:
+            n, m = self.n, self.m
+            # every rank must create every group, in the same order
+            ep = [dist.new_group([d * m + t for d in range(n)]) for t in range(m)]
+            tp = [dist.new_group([j * m + t for t in range(m)]) for j in range(n)]
+            self._ep_group = ep[self.tp_rank]
+            self._tp_group = tp[self.group]
+        return self._ep_group, self._tp_group
+
+    def forward_baseline(self, x, logits, stream=None, events=None):
+        """NCCL AR + A2A layout (sim:598-680): full-width all_to_all dispatch
+        from every TP rank, the same expert kernels, full-width all_to_all
+        combine of TP partials, TP all_reduce.  Needs the send counts on the
+        host (one D2H sync), as any NCCL all_to_all_single with splits does."""
+        p, r, lib = self.plan, self.rank, N.load()
+        s = stream or torch.cuda.current_stream()
+        sp = stream_ptr(s)
+        ep_g, tp_g = self._groups()
+
+        def mark(name):
+            if events is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                events.append((name, ev))
+
+        mark("start")
+        p.route(logits=logits, rank=r, stream=s)
+        p.barrier(stream=s)          # count rows published (our K1 exchange)
+        p.layout(rank=r, stream=s)
+        send = p.rank_views(r)["send"]
+        S = send.cpu().numpy()       # host sync for the split sizes
+        mark("route")
+        j, n, h = self.group, self.n, self.h
+        send_rows = int(S[j].sum())
+        sendbuf = torch.empty(max(1, send_rows), h, dtype=self.dtype, device=x.device)
+        cnt = torch.empty(n, dtype=torch.int32, device=x.device)
+        N.check(lib.mx_baseline_dispatch_pack(p._plan, r, C.c_void_p(x.data_ptr()),
+                                              C.c_void_p(sendbuf.data_ptr()),
+                                              C.c_void_p(cnt.data_ptr()), sp), "pack")
+        recv_rows = int(S[:, j].sum())
+        recvbuf = torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=x.device)
+        dist.all_to_all_single(recvbuf[:recv_rows], sendbuf[:send_rows],
+                               output_split_sizes=[int(v) for v in S[:, j]],
+                               input_split_sizes=[int(v) for v in S[j]],
+                               group=ep_g)
+        mark("a2a_dispatch")
+        N.check(lib.mx_baseline_dispatch_unpack(p._plan, r, C.c_void_p(recvbuf.data_ptr()),
+                                                sp), "unpack")
+        N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 0, sp), "expert")
+        mark("expert")
+        back = torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=x.device)
+        N.check(lib.mx_baseline_combine_pack(p._plan, r, C.c_void_p(back.data_ptr()),
+                                             C.c_void_p(cnt.data_ptr()), sp), "pack back")
+        ret = torch.empty(max(1, send_rows), h, dtype=self.dtype, device=x.device)
+        dist.all_to_all_single(ret[:send_rows], back[:recv_rows],
+                               output_split_sizes=[int(v) for v in S[j]],
+                               input_split_sizes=[int(v) for v in S[:, j]],
+                               group=ep_g)
+        mark("a2a_combine")
+        y = torch.empty(self.T, h, dtype=self.dtype, device=x.device)
+        N.check(lib.mx_baseline_combine_unpack(p._plan, r, C.c_void_p(ret.data_ptr()),
+                                               C.c_void_p(y.data_ptr()), sp), "unpack back")
+        if self.m > 1:
+            dist.all_reduce(y, group=tp_g)
+        mark("allreduce")
+        return y
+
+    def close(self):
+        self.plan.close()

@@ -84,7 +84,7 @@ class LayerPlan:
             N.check(lib.mx_comm_create(n, m, self.rank, 1 if emulate else 0,
                                        self.heap_bytes, C.byref(comm)), "comm")
         self._comm = comm
-        if not emulate:
+        if not emulate and self.W > 1:
             self._open_peers(process_group)
         plan = C.c_void_p()
         N.check(lib.mx_plan_create(comm, C.byref(self.desc), C.byref(plan)),

@@ -1,0 +1,119 @@
+"""Multi-GPU parity of the SPMD layer (one rank per GPU, NVLink peer heaps).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/spmd_check.py [--tp M]
+
+Checks, for the n x m cluster of the world size:
+  * f64 affine experts, explicit RouterSpec routing: fused output bit-exact
+    with the oracle's restatement of run_moe_block (sim:565-592);
+  * bf16 SwiGLU experts with the fused gate: within 2e-2 of the oracle;
+  * the NCCL AR+A2A baseline (sim:598-680) agrees with the oracle;
+  * repeated forwards are deterministic (device barrier epochs advance).
+Exit code 0 on success.
+"""
+import argparse
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle import mixserve_oracle as orc  # noqa: E402
+from paper_2601_08800_b200 import RouterSpec, SwiGLUExperts  # noqa: E402
+from paper_2601_08800_b200.layer import MoELayer, layout_for  # noqa: E402
+
+
+def gather_rows(y, world):
+    out = [torch.empty_like(y) for _ in range(world)]
+    dist.all_gather(out, y.contiguous())
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tp", type=int, default=None)
+    args = ap.parse_args()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n, m = layout_for(world, args.tp)
+    g, t = divmod(rank, m)
+    failures = []
+
+    # ---------------- f64 affine, explicit routing: bit-exact
+    T, h, E, k = 96, 72, 16, 4
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((n * T, h))
+    router = RouterSpec.random(n * T, E, k, seed=8)
+    ids, w = router.arrays()
+    scales = np.arange(1, E + 1, dtype=np.float64)
+    biases = np.arange(E, dtype=np.float64)
+    layer = MoELayer(n, m, T, h, E, k, 0, rank=rank, dtype=torch.float64,
+                     expert_kind="affine", scales=scales, biases=biases)
+    xs = torch.as_tensor(x[g * T:(g + 1) * T], device="cuda")
+    ids_d = torch.as_tensor(ids[g * T:(g + 1) * T], device="cuda").contiguous()
+    w_d = torch.as_tensor(w[g * T:(g + 1) * T], device="cuda").contiguous()
+    y1 = layer.forward(xs, ids=ids_d, weights=w_d).clone()
+    y2 = layer.forward(xs, ids=ids_d, weights=w_d).clone()
+    if not torch.equal(y1, y2):
+        failures.append("f64 affine: repeated forward differs")
+    ys = gather_rows(y1, world)
+    if rank == 0:
+        y_ref, _ = orc.run_fused_affine(n, m, x, ids, w, E, scales, biases)
+        for r in range(world):
+            gg = r // m
+            got = ys[r].cpu().numpy()
+            if not np.array_equal(got, y_ref[gg * T:(gg + 1) * T]):
+                err = np.abs(got - y_ref[gg * T:(gg + 1) * T]).max()
+                failures.append(f"f64 affine rank {r}: not bit-exact (max err {err:.3e})")
+    layer.close()
+
+    # ---------------- bf16 SwiGLU, fused gate
+    T, h, E, k, I = 128, 256, 32, 4, 512
+    ex = SwiGLUExperts.random(E, h, I, seed=3)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    x_all = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    l_all = torch.randn(n * T, E, device="cuda", generator=gen)
+    layer = MoELayer(n, m, T, h, E, k, I, experts=ex, rank=rank)
+    xs, ls = x_all[g * T:(g + 1) * T].contiguous(), l_all[g * T:(g + 1) * T].contiguous()
+    for _ in range(3):
+        y = layer.forward(xs, ls).clone()
+    y_bl = layer.forward_baseline(xs, ls).clone()
+    ys = gather_rows(y, world)
+    ybs = gather_rows(y_bl, world)
+    if rank == 0:
+        oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                               ex.w_down.float().cpu().numpy())
+        ids, w = orc.router_topk(l_all.cpu().numpy(), k)
+        y_ref = orc.moe_layer_swiglu(x_all.float().cpu().numpy(), ids, w, oex)
+        for r in range(world):
+            gg = r // m
+            ref = y_ref[gg * T:(gg + 1) * T]
+            e1 = orc.verify_metric(ys[r].float().cpu().numpy(), ref)
+            e2 = orc.verify_metric(ybs[r].float().cpu().numpy(), ref)
+            print(f"rank {r}: fused err {e1:.3e}, nccl-baseline err {e2:.3e}", flush=True)
+            if e1 > 2e-2:
+                failures.append(f"swiglu fused rank {r}: err {e1:.3e}")
+            if e2 > 2e-2:
+                failures.append(f"swiglu baseline rank {r}: err {e2:.3e}")
+    layer.close()
+
+    flag = torch.tensor([len(failures)], device="cuda")
+    dist.all_reduce(flag)
+    if rank == 0:
+        for f in failures:
+            print("FAIL:", f, flush=True)
+        print(f"spmd_check world={world} n={n} m={m}: "
+              f"{'OK' if flag.item() == 0 else 'FAILED'}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
