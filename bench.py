@@ -64,7 +64,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -74,7 +74,12 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.monotonic()
+        while self.proc and not self.lines and time.monotonic() - t0 < timeout:
+            time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.proc:
@@ -84,10 +89,14 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None, margin=0.25):
+        """Median SM clock and active throttle reasons of the samples taken
+        inside [t0 - margin, t1 + margin] (the timed region)."""
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for ts, ln in self.lines
+                 if t0 is None or (t0 - margin <= ts <= t1 + margin)]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -102,7 +111,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window": "timed region +-0.25 s"}
 
 
 # ------------------------------------------------------------------ CPU
@@ -200,8 +210,11 @@ def phase_model(S, cnt, n, m, group, tp, T):
         model["dispatch"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
         model["combine"] = {"bound": "hbm", "bytes": slots * hb + T * hb}
     else:
-        model["dispatch"] = {"bound": "nvlink", "bytes": remote_in * hb,
-                             "local_hbm_bytes": 2 * local_rows * hb}
+        if remote_in > 0:
+            model["dispatch"] = {"bound": "nvlink", "bytes": remote_in * hb,
+                                 "local_hbm_bytes": 2 * local_rows * hb}
+        else:   # one group (pure TP): every row is a local gather
+            model["dispatch"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
         # pulls: every slot's column shard from the m TP ranks of its host,
         # minus the one local read; plus the (m-1)/m of y pushed by TP peers
         own_host_slots = int(S[group, group])
@@ -256,13 +269,16 @@ def run_ours(args):
     # ---- timed region: K steps, per-phase events, L2 flushed in between
     per_step, phase_times = [], {}
     with ClockSampler(local) as clk:
+        clk.wait_first()
         sync_all()
+        t_region0 = time.monotonic()
         for _ in range(args.steps):
             flush.fill_(1)
             evs = []
             layer.forward_phases(x, logits, evs, stream=stream)
             per_step.append(evs)
         torch.cuda.synchronize()
+        t_region1 = time.monotonic()
     step_ms = []
     for evs in per_step:
         step_ms.append(evs[0][1].elapsed_time(evs[-1][1]))
@@ -376,7 +392,7 @@ def run_ours(args):
                        "global_tokens": T_GLOBAL, "groups_n": n, "tp_m": m,
                        "parallelism": f"TP{m}xEP{n}", "l2": "flushed (256 MiB write) between steps",
                        "weights": "random init, seed 0"},
-            "clocks": clk.summary(),
+            "clocks": clk.summary(t_region0, t_region1),
             "e2e": {"value": T_GLOBAL / (e2e_step / 1e3), "unit": "tokens/s",
                     "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
@@ -399,8 +415,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tp", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")

@@ -47,21 +47,30 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     // ---- fused softmax + top-k: one warp per token, lane owns experts
     //      e = 128*i + 4*lane + q (128-bit coalesced loads when aligned).
     const bool vec = (E % 4) == 0;
-    for (int tl = warp; tl < nt; tl += nw) {
+    // software-pipelined: the next token's logits are in flight while the
+    // current token's top-k runs (hides the DRAM latency of the row loads)
+    auto load_row = [&](int tl, float (&dst)[EV * 4]) {
       const float* row = logits + (size_t)(t0 + tl) * E;
-      float val[EV * 4];
 #pragma unroll
       for (int i = 0; i < EV; ++i) {
         const int e0 = 128 * i + 4 * lane;
         if (vec && e0 < E) {
           float4 f = __ldg(reinterpret_cast<const float4*>(row + e0));
-          val[4 * i] = f.x; val[4 * i + 1] = f.y; val[4 * i + 2] = f.z; val[4 * i + 3] = f.w;
+          dst[4 * i] = f.x; dst[4 * i + 1] = f.y; dst[4 * i + 2] = f.z; dst[4 * i + 3] = f.w;
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            val[4 * i + q] = (e0 + q < E) ? __ldg(row + e0 + q) : -INFINITY;
+            dst[4 * i + q] = (e0 + q < E) ? __ldg(row + e0 + q) : -INFINITY;
         }
       }
+    };
+    float nxt[EV * 4];
+    if (warp < nt) load_row(warp, nxt);
+    for (int tl = warp; tl < nt; tl += nw) {
+      float val[EV * 4];
+#pragma unroll
+      for (int i = 0; i < EV * 4; ++i) val[i] = nxt[i];
+      if (tl + nw < nt) load_row(tl + nw, nxt);
       unsigned taken = 0;
       int my_e = 0;
       float my_v = 0.f;
