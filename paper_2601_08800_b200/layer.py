@@ -88,16 +88,17 @@ class MoELayer:
         out.copy_(self.y, non_blocking=True)
         return out
 
-    def forward_phases(self, x, logits, events, stream=None):
+    def forward_phases(self, x, logits, events, stream=None, event_factory=None):
         """Same launches as :meth:`forward`, phase by phase, recording a CUDA
         event after each phase (for per-kernel timing in bench.py)."""
         p, r = self.plan, self.rank
         s = stream or torch.cuda.current_stream()
         lib = N.load()
         sp = stream_ptr(s)
+        make = event_factory or (lambda: torch.cuda.Event(enable_timing=True))
 
         def mark(name):
-            ev = torch.cuda.Event(enable_timing=True)
+            ev = make()
             ev.record(s)
             events.append((name, ev))
 
@@ -115,6 +116,11 @@ class MoELayer:
         p.combine(rank=r, stream=s); mark("combine")
         p.barrier(stream=s); mark("barrier_out")
         return self.y
+
+    def capture(self, x, logits=None, ids=None, weights=None, with_events=False):
+        """Capture one forward (all launches and device barriers) in a CUDA
+        graph bound to these input buffers; see :class:`CapturedForward`."""
+        return CapturedForward(self, x, logits, ids, weights, with_events)
 
     def routing_counts(self):
         """(cnt_all [n,E], send [n,n]) of the last forward, on the host."""
@@ -192,3 +198,48 @@ class MoELayer:
 
     def close(self):
         self.plan.close()
+
+
+class CapturedForward:
+    """A layer forward captured once and replayed as one CUDA graph.
+
+    Barrier epochs live on the device, so replays stay in lockstep across
+    ranks; inputs are read from the captured buffers (copy new tokens into
+    ``x``/``logits`` before calling).  ``with_events`` records an external
+    CUDA event after every phase inside the graph (per-kernel timing)."""
+
+    def __init__(self, layer, x, logits=None, ids=None, weights=None, with_events=False):
+        self.layer, self.x, self.logits = layer, x, logits
+        self.events = []
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):            # warm-up outside the graph
+            layer.forward(x, logits, ids=ids, weights=weights)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            if with_events:
+                evs = []
+                layer.forward_phases(x, logits, evs, event_factory=_external_event)
+                self.events = evs
+            else:
+                layer.forward(x, logits, ids=ids, weights=weights)
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+
+    def __call__(self):
+        self.graph.replay()
+        return self.layer.y
+
+    def phase_ms(self):
+        """(name, ms) per phase of the last replay (call after a sync)."""
+        return [(b, ea.elapsed_time(eb))
+                for (a, ea), (b, eb) in zip(self.events[:-1], self.events[1:])]
+
+
+def _external_event():
+    return torch.cuda.Event(enable_timing=True, external=True)

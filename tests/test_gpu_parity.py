@@ -294,3 +294,31 @@ def test_swiglu_layer_vs_oracle(shape):
     # the package's own dense GPU oracle agrees with the CPU one
     y_d = moe_oracle(x, router, ex)
     assert orc.verify_metric(y_d.double().cpu().numpy(), y_o) <= 1e-3
+
+
+# ----------------------------------------------------------------- SPMD layer, 1 GPU
+def test_layer_graph_replay_matches_eager_and_oracle():
+    from paper_2601_08800_b200 import SwiGLUExperts
+    from paper_2601_08800_b200.layer import MoELayer
+    T, h, E, k, I = 512, 256, 32, 4, 256
+    ex = SwiGLUExperts.random(E, h, I, seed=9)
+    layer = MoELayer(1, 1, T, h, E, k, I, experts=ex, rank=0)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = torch.randn(T, E, device="cuda", generator=gen)
+    y_eager = layer.forward(x, logits).clone()
+    run = layer.capture(x, logits, with_events=True)
+    for _ in range(3):
+        y_g = run().clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y_g, y_eager)
+    assert [n for n, _ in run.phase_ms()][0] == "route"
+    # new tokens copied into the captured buffers
+    x.copy_(torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16))
+    y2 = run().clone()
+    oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
+    assert orc.verify_metric(y2.float().cpu().numpy(), y_o) <= 2e-2
+    layer.close()
