@@ -18,8 +18,92 @@
 
 namespace mx {
 
-// One CTA per chunk of MX_CHUNK tokens of this rank's group.
+// Fused softmax + top-k gate: one warp per token over all SMs.  Lane owns
+// experts e = 128*i + 4*lane + q (128-bit coalesced row loads).  Selection
+// key: fp32 logit descending, lowest id on ties (exact compares, so ids are
+// bit-exact with the oracle).  Each lane caches its best untaken candidate;
+// only the winning lane rescans, so a round is one 5-level warp argmax.
 template <class WT, int EV>
+__global__ void __launch_bounds__(256)
+k_gate(DevView v, const float* __restrict__ logits) {
+  const int lane = threadIdx.x & 31;
+  const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (tok >= v.T) return;
+  const int E = v.E, k = v.k;
+  int* ids = at<int>(v, v.rank, v.off.ids);
+  WT* w = at<WT>(v, v.rank, v.off.w);
+  const float* row = logits + (size_t)tok * E;
+  float val[EV * 4];
+#pragma unroll
+  for (int i = 0; i < EV; ++i) {
+    const int e0 = 128 * i + 4 * lane;
+    if ((E % 4) == 0 && e0 < E) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(row + e0));
+      val[4 * i] = f.x; val[4 * i + 1] = f.y; val[4 * i + 2] = f.z; val[4 * i + 3] = f.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) val[4 * i + q] = (e0 + q < E) ? __ldg(row + e0 + q) : -INFINITY;
+    }
+  }
+  unsigned taken = 0;
+  float cv;
+  int ce;
+  auto rescan = [&]() {
+    cv = -INFINITY;
+    ce = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < EV * 4; ++i) {
+      const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+      if (e < E && !((taken >> i) & 1u) && (val[i] > cv || (val[i] == cv && e < ce))) {
+        cv = val[i];
+        ce = e;
+      }
+    }
+  };
+  rescan();
+  int my_e = 0;
+  float my_v = 0.f;
+  for (int r = 0; r < k; ++r) {
+    float bv = cv;
+    int be = ce;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+    }
+    if (lane == r) { my_e = be; my_v = bv; }
+    if (be == ce) {  // this lane owned the winner
+      taken |= 1u << (4 * (be >> 7) + (be & 3));
+      rescan();
+    }
+  }
+  const float mx = __shfl_sync(0xffffffffu, my_v, 0);  // top-1 = row max
+  const float ex = (lane < k) ? expf(my_v - mx) : 0.f;
+  float denom;
+  if (v.renorm) {
+    denom = ex;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+  } else {
+    float sacc = 0.f;
+#pragma unroll
+    for (int i = 0; i < EV * 4; ++i) {
+      const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+      if (e < E) sacc += expf(val[i] - mx);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    denom = sacc;
+  }
+  if (lane < k) {
+    ids[(size_t)tok * k + lane] = my_e;
+    w[(size_t)tok * k + lane] = (WT)(ex / denom);
+  }
+}
+
+// One CTA per chunk of MX_CHUNK tokens of this rank's group.
+template <class WT>
 __global__ void __launch_bounds__(512)
 k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__ ids_in,
         const WT* __restrict__ w_in) {
@@ -30,6 +114,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
   int* s_ids = reinterpret_cast<int*>(smem);                      // [CHUNK*k]
   unsigned* s_mask = reinterpret_cast<unsigned*>(s_ids + MX_CHUNK * k);  // [E][4]
   int* s_hc = reinterpret_cast<int*>(s_mask + E * 4);             // [CHUNK][n]
+  int* s_home = s_hc + MX_CHUNK * n;                              // [E]
 
   int* ids = at<int>(v, v.rank, v.off.ids);
   WT* w = at<WT>(v, v.rank, v.off.w);
@@ -42,81 +127,11 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
 
   for (int i = threadIdx.x; i < E * 4; i += blockDim.x) s_mask[i] = 0;
   for (int i = threadIdx.x; i < MX_CHUNK * n; i += blockDim.x) s_hc[i] = 0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_home[e] = home_of(e, n, E);
 
   if (logits != nullptr) {
-    // ---- fused softmax + top-k: one warp per token, lane owns experts
-    //      e = 128*i + 4*lane + q (128-bit coalesced loads when aligned).
-    const bool vec = (E % 4) == 0;
-    // software-pipelined: the next token's logits are in flight while the
-    // current token's top-k runs (hides the DRAM latency of the row loads)
-    auto load_row = [&](int tl, float (&dst)[EV * 4]) {
-      const float* row = logits + (size_t)(t0 + tl) * E;
-#pragma unroll
-      for (int i = 0; i < EV; ++i) {
-        const int e0 = 128 * i + 4 * lane;
-        if (vec && e0 < E) {
-          float4 f = __ldg(reinterpret_cast<const float4*>(row + e0));
-          dst[4 * i] = f.x; dst[4 * i + 1] = f.y; dst[4 * i + 2] = f.z; dst[4 * i + 3] = f.w;
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            dst[4 * i + q] = (e0 + q < E) ? __ldg(row + e0 + q) : -INFINITY;
-        }
-      }
-    };
-    float nxt[EV * 4];
-    if (warp < nt) load_row(warp, nxt);
-    for (int tl = warp; tl < nt; tl += nw) {
-      float val[EV * 4];
-#pragma unroll
-      for (int i = 0; i < EV * 4; ++i) val[i] = nxt[i];
-      if (tl + nw < nt) load_row(tl + nw, nxt);
-      unsigned taken = 0;
-      int my_e = 0;
-      float my_v = 0.f;
-      for (int r = 0; r < k; ++r) {
-        float bv = -INFINITY;
-        int be = 0x7fffffff;
-#pragma unroll
-        for (int i = 0; i < EV * 4; ++i) {
-          const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
-          const bool ok = e < E && !((taken >> i) & 1u);
-          if (ok && (val[i] > bv || (val[i] == bv && e < be))) { bv = val[i]; be = e; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          int oe = __shfl_xor_sync(0xffffffffu, be, o);
-          if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
-        }
-        if (((be & 127) >> 2) == lane) taken |= 1u << (4 * (be >> 7) + (be & 3));
-        if (lane == r) { my_e = be; my_v = bv; }
-      }
-      const float mx = __shfl_sync(0xffffffffu, my_v, 0);  // top-1 = row max
-      float ex = (lane < k) ? expf(my_v - mx) : 0.f;
-      float denom;
-      if (v.renorm) {
-        denom = ex;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
-      } else {
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < EV * 4; ++i) {
-          const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
-          if (e < E) s += expf(val[i] - mx);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        denom = s;
-      }
-      if (lane < k) {
-        const size_t si = (size_t)(t0 + tl) * k + lane;
-        ids[si] = my_e;
-        w[si] = (WT)(ex / denom);
-        s_ids[tl * k + lane] = my_e;
-      }
-    }
+    // gate already ran (k_gate): ids/weights are in this rank's buffers
+    for (int i = threadIdx.x; i < nt * k; i += blockDim.x) s_ids[i] = ids[(size_t)t0 * k + i];
   } else {
     // ---- explicit routing (RouterSpec ids/weights, sim:143-166)
     for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
@@ -143,14 +158,14 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     const int tl = threadIdx.x;
     for (int i = 0; i < k; ++i) {
       const int e = s_ids[tl * k + i];
-      const int d = home_of(e, n, E);
+      const int d = s_home[e];
       int rk = 0;
       for (int wd = 0; wd < (tl >> 5); ++wd) rk += __popc(s_mask[e * 4 + wd]);
       rk += __popc(s_mask[e * 4 + (tl >> 5)] & ((1u << (tl & 31)) - 1u));
       int within = 0;  // experts of this token on host d with a smaller id
       for (int i2 = 0; i2 < k; ++i2) {
         const int e2 = s_ids[tl * k + i2];
-        within += (e2 < e && home_of(e2, n, E) == d) ? 1 : 0;
+        within += (e2 < e && s_home[e2] == d) ? 1 : 0;
       }
       const size_t si = (size_t)(t0 + tl) * k + i;
       slot_rank[si] = rk;
@@ -189,7 +204,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     for (int i = 0; i < k; ++i) {
       const int e = s_ids[tl * k + i];
       const size_t si = (size_t)(t0 + tl) * k + i;
-      slot_tmr[si] += s_hc[tl * n + home_of(e, n, E)];
+      slot_tmr[si] += s_hc[tl * n + s_home[e]];
     }
   }
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -323,33 +338,36 @@ __global__ void k_slotpos(DevView v) {
 }
 
 template <class WT, int EV>
-static int launch_route_ev(const DevView& v, int C, size_t smem, const float* logits,
-                           const int32_t* ids, const void* w, cudaStream_t s) {
-  auto kern = k_route<WT, EV>;
-  static bool attr = false;
-  if (!attr) {
-    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  kern<<<C, 512, smem, s>>>(v, logits, ids, static_cast<const WT*>(w));
-  MX_LAUNCH_CHECK();
-  return MX_OK;
+static void launch_gate_ev(const DevView& v, const float* logits, cudaStream_t s) {
+  k_gate<WT, EV><<<(v.T + 7) / 8, 256, 0, s>>>(v, logits);
 }
 
 template <class WT>
 static int launch_route_wt(const DevView& v, int C, size_t smem, const float* logits,
                            const int32_t* ids, const void* w, cudaStream_t s) {
-  if (v.E <= 128) return launch_route_ev<WT, 1>(v, C, smem, logits, ids, w, s);
-  if (v.E <= 256) return launch_route_ev<WT, 2>(v, C, smem, logits, ids, w, s);
-  if (v.E <= 512) return launch_route_ev<WT, 4>(v, C, smem, logits, ids, w, s);
-  return launch_route_ev<WT, 8>(v, C, smem, logits, ids, w, s);
+  if (logits) {
+    if (v.E <= 128) launch_gate_ev<WT, 1>(v, logits, s);
+    else if (v.E <= 256) launch_gate_ev<WT, 2>(v, logits, s);
+    else if (v.E <= 512) launch_gate_ev<WT, 4>(v, logits, s);
+    else launch_gate_ev<WT, 8>(v, logits, s);
+    MX_LAUNCH_CHECK();
+  }
+  static bool attr = false;
+  if (!attr) {
+    MX_CUDA(cudaFuncSetAttribute(k_route<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_route<WT><<<C, 512, smem, s>>>(v, logits, ids, static_cast<const WT*>(w));
+  MX_LAUNCH_CHECK();
+  return MX_OK;
 }
 
 int launch_route(const DevView& v, const float* logits, const int32_t* ids,
                  const void* w, cudaStream_t s) {
   const int C = v.C;
   if (C == 0) return MX_OK;
-  const size_t smem = (size_t)MX_CHUNK * v.k * 4 + (size_t)v.E * 16 + (size_t)MX_CHUNK * v.n * 4;
+  const size_t smem = (size_t)MX_CHUNK * v.k * 4 + (size_t)v.E * 16 + (size_t)MX_CHUNK * v.n * 4 +
+                      (size_t)v.E * 4;
   int rc = v.elt == 8 ? launch_route_wt<double>(v, C, smem, logits, ids, w, s)
                       : launch_route_wt<float>(v, C, smem, logits, ids, w, s);
   if (rc) return rc;
