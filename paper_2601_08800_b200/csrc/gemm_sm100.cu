@@ -167,18 +167,34 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   uint64_t* tempty = tfull + 2;         // [2]
   __shared__ uint32_t s_tmem;
   __shared__ int s_tstart[MX_EMAX + 1];
+  __shared__ int s_off[MX_EMAX];
+  __shared__ int s_cnt[MX_EMAX];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = args.G, nN = args.N / BN, kblocks = args.K / BK;
 
-  // per-group tile prefix (G <= MX_EMAX)
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int g = 0; g < G; ++g) {
-      s_tstart[g] = run;
-      run += ((args.cnts[g] + BM - 1) / BM) * nN;
+  // group offsets/counts -> smem (parallel loads), then the per-group tile
+  // prefix by one warp-scan pass (G <= MX_EMAX); no per-tile global reads
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    s_off[g] = args.offs[g];
+    s_cnt[g] = args.cnts[g];
+  }
+  __syncthreads();
+  if (warp == 3) {
+    int carry = 0;
+    for (int base = 0; base < G; base += 32) {
+      const int g = base + lane;
+      const int tiles = g < G ? ((s_cnt[g] + BM - 1) / BM) * nN : 0;
+      int incl = tiles;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (g < G) s_tstart[g] = carry + incl - tiles;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    s_tstart[G] = run;
+    if (lane == 0) s_tstart[G] = carry;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -215,7 +231,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int g, mb, nb;
         decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
-        const int a_row = args.offs[g] + mb * BM;
+        const int a_row = s_off[g] + mb * BM;
         const int bg = args.b_index ? args.b_index[g] : g;
         const int b_row = bg * args.N + nb * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -265,10 +281,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       int g, mb, nb;
       decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
-      const int cnt = args.cnts[g];
+      const int cnt = s_cnt[g];
       const int r_local = mb * BM + row_in_tile;
       const bool valid = r_local < cnt;
-      const long long row = (long long)args.offs[g] + r_local;
+      const long long row = (long long)s_off[g] + r_local;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
