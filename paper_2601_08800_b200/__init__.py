@@ -11,6 +11,14 @@ __version__ = "0.1.0"
 from .errors import (AnalyzerError, CalibrationError, CapacityError,  # noqa: F401
                      ConfigError, GrammarError, MoeplanError, SaturationError,
                      SchedulingError, StrategyError, VerificationError)
+from .analyzer import (ProfilingObservation, RankedStrategies, calibrate,  # noqa: F401
+                       compare_report, select_strategy)
+from .config import (CalibrationCoefficients, ClusterConfig, ConfigBundle,  # noqa: F401
+                     ModelHyperparams, WorkloadSpec, load_config)
+from .costmodel import (CostEstimate, indicators, lambda_ep_baseline,  # noqa: F401
+                        lambda_mix)
+from .strategy import (ParallelStrategy, check_memory, enumerate_strategies,  # noqa: F401
+                       format_strategy, parse_strategy)
 from .simcluster import (ExpertSpec, RouterSpec, SimCluster, SwiGLUExperts,  # noqa: F401
                          TraceEvent, build_cluster, build_routing_table,
                          fused_ag_dispatch, fused_rs_combine, moe_oracle,
@@ -18,6 +26,12 @@ from .simcluster import (ExpertSpec, RouterSpec, SimCluster, SwiGLUExperts,  # n
 
 __all__ = [
     "__version__",
+    "CalibrationCoefficients", "ClusterConfig", "ConfigBundle", "CostEstimate",
+    "ModelHyperparams", "ParallelStrategy", "ProfilingObservation",
+    "RankedStrategies", "WorkloadSpec", "calibrate", "check_memory",
+    "compare_report", "enumerate_strategies", "format_strategy", "indicators",
+    "lambda_ep_baseline", "lambda_mix", "load_config", "parse_strategy",
+    "select_strategy",
     "AnalyzerError", "CalibrationError", "CapacityError", "ConfigError",
     "ExpertSpec", "GrammarError", "MoeplanError", "RouterSpec",
     "SaturationError", "SchedulingError", "SimCluster", "StrategyError",
