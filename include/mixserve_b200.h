@@ -49,6 +49,12 @@ extern "C" {
 
 typedef enum { MX_F64 = 0, MX_F32 = 1, MX_BF16 = 2 } mx_dtype;
 typedef enum { MX_EXPERT_AFFINE = 0, MX_EXPERT_SWIGLU = 1 } mx_expert_kind;
+/* Wire format between groups.  SLOT: one row per routed slot both ways, the
+ * reference's A2A layout (sim:366-369, sim:458-475).  TOKEN: one row per
+ * (token, host group) pair -- dispatch dedup and combine pre-reduced per
+ * (token, host) before the pull; the routing tables and
+ * send/recv slot lists are identical, only the bytes on NVLink shrink.   */
+typedef enum { MX_WIRE_SLOT = 0, MX_WIRE_TOKEN = 1 } mx_wire;
 
 /* Buffers a plan exposes (for zero-copy views and parity inspection). */
 typedef enum {
@@ -64,7 +70,9 @@ typedef enum {
   MX_BUF_EXP_CNT = 9,  /* [E] int32: rows of each expert summed over groups  */
   MX_BUF_SEND = 10,    /* [n, n] int32: S[j][d] slots of group j on host d   */
   MX_BUF_ACT = 11,     /* [capacity, I/tp] bf16: SwiGLU activation           */
-  MX_BUF_COUNT_ = 12
+  MX_BUF_UPOS = 12,    /* [T, n] int32: (token, host) pair row in host's XBUF */
+  MX_BUF_XBUF = 13,    /* [T*n, h] act: deduplicated rows (wire TOKEN)       */
+  MX_BUF_COUNT_ = 14
 } mx_buffer;
 
 typedef struct mx_comm mx_comm;
@@ -81,6 +89,7 @@ typedef struct {
   int act_dtype;      /* mx_dtype of hidden states on the wire               */
   int expert_kind;    /* mx_expert_kind                                      */
   int renormalize;    /* top-k weights renormalised over the k (logits mode) */
+  int wire;           /* mx_wire                                             */
   long long capacity; /* receive rows per host; <=0: worst case T*n*min(k,E/n+1) */
 } mx_plan_desc;
 
@@ -148,7 +157,9 @@ MX_API int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream);
  * (affine stand-in sim:535-562, or the SwiGLU grouped GEMM).             */
 MX_API int mx_expert(mx_plan* p, int rank, const mx_expert_params* ep, void* stream);
 /* The same expert compute split in its launches, for per-kernel timing:
- * stage 1 = GEMM1 + SwiGLU epilogue, stage 2 = GEMM2, 0 = both.          */
+ * 0 = everything below in order; 1 = GEMM1 + SwiGLU epilogue (or the affine
+ * kernel); 2 = GEMM2; 3 = wire-TOKEN expand (XBUF -> RECV); 4 = wire-TOKEN
+ * pair pre-reduction (PARTIAL -> z).  0 runs 3, 1, 2, 4.                 */
 MX_API int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
                            void* stream);
 /* K4 fused RS-combine (sim:410-521): the owner pulls its column shard of

@@ -87,6 +87,7 @@ static int validate(const mx_plan_desc& d) {
   if (d.top_k < 1 || d.top_k > d.num_experts) { set_error("top_k must be in [1, num_experts]"); return MX_ERR_INVALID; }
   if (d.top_k > MX_KMAX) { set_error("top_k %d exceeds %d", d.top_k, MX_KMAX); return MX_ERR_UNSUPPORTED; }
   if (d.act_dtype < MX_F64 || d.act_dtype > MX_BF16) { set_error("bad act_dtype"); return MX_ERR_INVALID; }
+  if (d.wire != MX_WIRE_SLOT && d.wire != MX_WIRE_TOKEN) { set_error("bad wire format"); return MX_ERR_INVALID; }
   if (d.expert_kind == MX_EXPERT_SWIGLU) {
     if (d.act_dtype != MX_BF16) { set_error("SwiGLU experts run in bf16"); return MX_ERR_UNSUPPORTED; }
     if (d.inter % d.tp != 0 || (d.inter / d.tp) % 128 != 0) { set_error("inter/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED; }
@@ -95,6 +96,11 @@ static int validate(const mx_plan_desc& d) {
     set_error("bad expert_kind"); return MX_ERR_INVALID;
   }
   return MX_OK;
+}
+
+static int kh_of(const mx_plan_desc& d) {
+  const int per_host = (d.num_experts + d.n_group - 1) / d.n_group;
+  return d.top_k < per_host ? d.top_k : per_host;
 }
 
 static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
@@ -128,6 +134,21 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   o.send = take(4 * n * n);
   o.tm_off = take(4 * n * n);
   o.host_rows = take(4 * n);
+  o.ucnt_all = take(4 * n * n);
+  o.poff = take(4 * n * n);
+  o.host_pairs = take(4 * n);
+  o.chunk_pair = take(4 * C * n);
+  o.tok_pair_rank = take(4 * T * n);
+  o.upos = take(4 * T * n);
+  const bool tok = d.wire == MX_WIRE_TOKEN;
+  const size_t U = tok ? T * n : 0;
+  const size_t KH = kh_of(d);
+  o.xbuf = take(U * h * elt);
+  o.recv_src = take(tok ? 4 * (size_t)cap : 0);
+  o.pair_p = take(4 * U * KH);
+  o.pair_w = take(wsz * U * KH);
+  o.pair_n = take(4 * U);
+  o.z = take(U * h * elt);
   o.total = p;
   return o;
 }
@@ -275,6 +296,8 @@ int mx_plan_create(mx_comm* c, const mx_plan_desc* d, mx_plan** out) {
   v.C = (d->tokens + MX_CHUNK - 1) / MX_CHUNK;
   v.elt = elt_bytes(d->act_dtype);
   v.renorm = d->renormalize;
+  v.wire = d->wire;
+  v.KH = kh_of(*d);
   v.cap = p->cap;
   v.off = p->off;
   for (int r = 0; r < c->W; ++r) v.heap[r] = c->heap[r];
@@ -309,6 +332,8 @@ int mx_plan_buffer(mx_plan* p, int rank, int which, void** ptr, size_t* bytes) {
     case MX_BUF_EXP_CNT: off = o.exp_cnt; len = 4 * E; break;
     case MX_BUF_SEND: off = o.send; len = 4 * n * n; break;
     case MX_BUF_ACT: off = o.act; len = p->cap * (size_t)p->base.I_t * 2; break;
+    case MX_BUF_UPOS: off = o.upos; len = 4 * T * n; break;
+    case MX_BUF_XBUF: off = o.xbuf; len = (d.wire == MX_WIRE_TOKEN ? T * n : 0) * h * elt; break;
     default: set_error("bad buffer id %d", which); return MX_ERR_INVALID;
   }
   *ptr = p->comm->heap[rank] + off;
@@ -429,7 +454,8 @@ int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream) {
   const size_t row = (size_t)p->d.hidden * elt_bytes(p->d.act_dtype);
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
-    rc = launch_dispatch(v, group_ptr(p, x, v.group, row), s);
+    rc = p->d.wire == MX_WIRE_TOKEN ? launch_dispatch_token(v, group_ptr(p, x, v.group, row), s)
+                                    : launch_dispatch(v, group_ptr(p, x, v.group, row), s);
     if (rc) return rc;
   }
   return MX_OK;
@@ -439,13 +465,18 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
   RankIter it;
   int rc = ranks_for(p, rank, &it);
   if (rc) return rc;
-  if (stage < 0 || stage > 2) { set_error("stage must be 0, 1 or 2"); return MX_ERR_INVALID; }
+  if (stage < 0 || stage > 4) { set_error("stage must be in [0, 4]"); return MX_ERR_INVALID; }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
+    const bool tok = p->d.wire == MX_WIRE_TOKEN;
+    if (tok && (stage == 0 || stage == 3) && (rc = launch_expand(v, s))) return rc;
+    if (stage == 3 || stage == 4) {
+      if (tok && stage == 4 && (rc = launch_pair_reduce(v, s))) return rc;
+      continue;
+    }
     if (p->d.expert_kind == MX_EXPERT_AFFINE) {
-      if (stage == 2) continue;  // single-kernel expert
-      rc = launch_expert_affine(v, ep->scales, ep->biases, s);
+      if (stage != 2) rc = launch_expert_affine(v, ep->scales, ep->biases, s);
     } else {
       // emulated: per-rank weight shards stacked rank-major
       const int Elmax = (v.E + v.n - 1) / v.n;
@@ -456,6 +487,7 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
                                 static_cast<const char*>(ep->w2) + slot * w2_rank, stage, s);
     }
     if (rc) return rc;
+    if (tok && stage == 0 && (rc = launch_pair_reduce(v, s))) return rc;
   }
   return MX_OK;
 }
@@ -470,7 +502,8 @@ int mx_combine(mx_plan* p, int rank, void* y_out, void* stream) {
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int r = it.first; r < it.last; ++r) {
-    rc = launch_combine(view_for(p, r), s);
+    rc = p->d.wire == MX_WIRE_TOKEN ? launch_combine_token(view_for(p, r), s)
+                                    : launch_combine(view_for(p, r), s);
     if (rc) return rc;
   }
   if (y_out) {

@@ -54,6 +54,19 @@ struct Offsets {
   size_t send;        // int32 [n][n]
   size_t tm_off;      // int32 [n][n]
   size_t host_rows;   // int32 [n]
+  // (token, host) pairs -- wire TOKEN (dispatch dedup / pre-reduced combine)
+  size_t ucnt_all;    // int32 [n][n]  U[j][d]: tokens of group j with an expert on d (symmetric)
+  size_t poff;        // int32 [n][n]  exclusive over j of U[j][d]
+  size_t host_pairs;  // int32 [n]
+  size_t chunk_pair;  // int32 [n][C]  -> exclusive chunk base after route
+  size_t tok_pair_rank;  // int32 [T][n] rank among chunk tokens hitting d (-1: none)
+  size_t upos;        // int32 [T][n]  row of (token, d) in d's xbuf (-1: none)
+  size_t xbuf;        // act [T*n][h]  deduplicated rows (peers write)
+  size_t recv_src;    // int32 [cap]   xbuf row of every expert-major row (peers write)
+  size_t pair_p;      // int32 [T*n][KH] slot rows of a pair (peers write)
+  size_t pair_w;      // AccT [T*n][KH]  slot weights of a pair (peers write)
+  size_t pair_n;      // int32 [T*n]     slots of a pair (peers write)
+  size_t z;           // act [T*n][h]  pre-reduced w*partial per pair (peers read)
   size_t counters;    // int32 [16]  [0]=route CTA counter [2..3]=u64 barrier epoch
   size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
   size_t total;
@@ -64,6 +77,8 @@ struct DevView {
   int T, h, E, k, I_t, C;
   int elt;            // bytes per hidden element on the wire
   int renorm;
+  int wire;           // mx_wire
+  int KH;             // max slots of one token on one host
   long long cap;
   Offsets off;
   char* heap[MX_MAXW];
@@ -151,6 +166,10 @@ int launch_expert_affine(const DevView& v, const void* scales, const void* biase
 int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
                          cudaStream_t s);
 int launch_combine(const DevView& v, cudaStream_t s);
+int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s);
+int launch_expand(const DevView& v, cudaStream_t s);
+int launch_pair_reduce(const DevView& v, cudaStream_t s);
+int launch_combine_token(const DevView& v, cudaStream_t s);
 int launch_barrier(const DevView& v, cudaStream_t s);
 int launch_baseline_dispatch_pack(const DevView& v, const void* x, void* send,
                                   int32_t* counts, cudaStream_t s);

@@ -115,6 +115,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
   unsigned* s_mask = reinterpret_cast<unsigned*>(s_ids + MX_CHUNK * k);  // [E][4]
   int* s_hc = reinterpret_cast<int*>(s_mask + E * 4);             // [CHUNK][n]
   int* s_home = s_hc + MX_CHUNK * n;                              // [E]
+  int* s_hp = s_home + E;                                         // [CHUNK][n]
 
   int* ids = at<int>(v, v.rank, v.off.ids);
   WT* w = at<WT>(v, v.rank, v.off.w);
@@ -122,6 +123,8 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
   int* slot_tmr = at<int>(v, v.rank, v.off.slot_tmr);
   int* chunk_hist = at<int>(v, v.rank, v.off.chunk_hist);
   int* chunk_host = at<int>(v, v.rank, v.off.chunk_host);
+  int* chunk_pair = at<int>(v, v.rank, v.off.chunk_pair);
+  int* tok_pair_rank = at<int>(v, v.rank, v.off.tok_pair_rank);
   int* err = at<int>(v, v.rank, v.off.err);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 
@@ -174,29 +177,39 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     }
   }
   __syncthreads();
-  // exclusive scan of host counts over the chunk's tokens (4 per lane)
+  // exclusive scans over the chunk's tokens (4 per lane) of (a) the slot
+  // counts per host (token-major table index) and (b) the indicator "token
+  // has an expert on host d" ((token, host) pair index, wire TOKEN)
   for (int d = warp; d < n; d += nw) {
-    int a[4], run = 0;
+    int a[4], run = 0, pa[4], prun = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int tl = 4 * lane + q;
       a[q] = (tl < nt) ? s_hc[tl * n + d] : 0;
+      pa[q] = a[q] > 0 ? 1 : 0;
       run += a[q];
+      prun += pa[q];
     }
-    int incl = run;
+    int incl = run, pincl = prun;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      const int py = __shfl_up_sync(0xffffffffu, pincl, o);
+      if (lane >= o) { incl += y; pincl += py; }
     }
-    int ex = incl - run;
+    int ex = incl - run, pex = pincl - prun;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int tl = 4 * lane + q;
-      if (tl < MX_CHUNK) s_hc[tl * n + d] = ex;
+      s_hc[tl * n + d] = ex;
+      s_hp[tl * n + d] = pa[q] ? pex : -1;
       ex += a[q];
+      pex += pa[q];
     }
-    if (lane == 31) chunk_host[d * v.C + c] = incl;
+    if (lane == 31) {
+      chunk_host[d * v.C + c] = incl;
+      chunk_pair[d * v.C + c] = pincl;
+    }
   }
   __syncthreads();
   if (threadIdx.x < nt) {
@@ -206,6 +219,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
       const size_t si = (size_t)(t0 + tl) * k + i;
       slot_tmr[si] += s_hc[tl * n + s_home[e]];
     }
+    for (int d = 0; d < n; ++d) tok_pair_rank[(size_t)(t0 + tl) * n + d] = s_hp[tl * n + d];
   }
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     chunk_hist[e * v.C + c] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
@@ -223,6 +237,7 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
   int* row;
   if (w < E) row = at<int>(v, v.rank, v.off.chunk_hist) + (size_t)w * C;
   else if (w < E + n) row = at<int>(v, v.rank, v.off.chunk_host) + (size_t)(w - E) * C;
+  else if (w < E + 2 * n) row = at<int>(v, v.rank, v.off.chunk_pair) + (size_t)(w - E - n) * C;
   else return;
   int carry = 0;
   for (int base = 0; base < C; base += 32) {
@@ -242,6 +257,10 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
   }
   if (w < E && v.W > 32) {
     for (int r = 32 + lane; r < v.W; r += 32) at<int>(v, r, v.off.cnt_all)[v.group * E + w] = carry;
+  }
+  if (w >= E + n) {  // (token, host) pair totals U[group][d], published like the counts
+    const int d = w - E - n;
+    for (int r = lane; r < v.W; r += 32) at<int>(v, r, v.off.ucnt_all)[v.group * n + d] = carry;
   }
 }
 
@@ -298,6 +317,18 @@ __global__ void __launch_bounds__(1024) k_layout_meta(DevView v) {
     for (int j2 = 0; j2 < j; ++j2) s += s_send[j2 * n + d];
     tm_off[jd] = s;
   }
+  {
+    const int* ucnt = at<int>(v, v.rank, v.off.ucnt_all);
+    int* poff = at<int>(v, v.rank, v.off.poff);
+    int* hp = at<int>(v, v.rank, v.off.host_pairs);
+    for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
+      const int j = jd / n, d = jd % n;
+      int s = 0;
+      for (int j2 = 0; j2 < j; ++j2) s += ucnt[j2 * n + d];
+      poff[jd] = s;
+      if (j == n - 1) hp[d] = s + ucnt[jd];
+    }
+  }
   for (int d = threadIdx.x; d < n; d += blockDim.x) {
     int s = 0;
     for (int j = 0; j < n; ++j) s += s_send[j * n + d];
@@ -335,6 +366,18 @@ __global__ void k_slotpos(DevView v) {
     slot_pos[s] = (int)pos;
     slot_tm[s] = tm;
   }
+  // (token, host) pair rows in the host's deduplicated buffer
+  const int* tpr = at<int>(v, v.rank, v.off.tok_pair_rank);
+  const int* chunk_pair = at<int>(v, v.rank, v.off.chunk_pair);
+  const int* poff = at<int>(v, v.rank, v.off.poff);
+  int* upos = at<int>(v, v.rank, v.off.upos);
+  const long long tn = (long long)v.T * n;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < tn;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(q / n), d = (int)(q % n);
+    const int r = tpr[q];
+    upos[q] = r < 0 ? -1 : poff[v.group * n + d] + chunk_pair[d * v.C + t / MX_CHUNK] + r;
+  }
 }
 
 template <class WT, int EV>
@@ -366,12 +409,12 @@ int launch_route(const DevView& v, const float* logits, const int32_t* ids,
                  const void* w, cudaStream_t s) {
   const int C = v.C;
   if (C == 0) return MX_OK;
-  const size_t smem = (size_t)MX_CHUNK * v.k * 4 + (size_t)v.E * 16 + (size_t)MX_CHUNK * v.n * 4 +
+  const size_t smem = (size_t)MX_CHUNK * v.k * 4 + (size_t)v.E * 16 + (size_t)MX_CHUNK * v.n * 8 +
                       (size_t)v.E * 4;
   int rc = v.elt == 8 ? launch_route_wt<double>(v, C, smem, logits, ids, w, s)
                       : launch_route_wt<float>(v, C, smem, logits, ids, w, s);
   if (rc) return rc;
-  const int warps = v.E + v.n;
+  const int warps = v.E + 2 * v.n;
   k_route_scan<<<(warps + 7) / 8, 256, 0, s>>>(v);
   MX_LAUNCH_CHECK();
   return MX_OK;

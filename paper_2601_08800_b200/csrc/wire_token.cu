@@ -1,0 +1,256 @@
+// wire_token.cu -- TOKEN wire format: one row per (token, host group) pair.
+//
+// The reference ships one row per routed slot in both directions: a token
+// routed to several experts of the same remote group crosses the link once
+// per expert (sim:366-369, sim:403-405), and the combine
+// returns one TP-reduced row per slot (sim:458-475).  The routing table, the
+// per-(src, dst) slot lists and the send counts stay exactly the reference's
+// (K1 computes them); only the bytes on NVLink change:
+//   dispatch: each (token, host) row crosses NVLink once into the host's
+//             XBUF; the host expands XBUF rows into its expert-major RECV
+//             (local HBM copy) before the grouped GEMM;
+//   combine:  each host TP rank pre-reduces z[u] = sum_i w_i * partial[p_i]
+//             over the token's slots on that host (experts ascending), and
+//             the owner pulls one z row shard per (host, TP rank).
+// NVLink bytes per token drop from k rows to (#hosts hit) rows each way.
+#include "mx_internal.cuh"
+
+namespace mx {
+
+__device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbytes, int lane) {
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | nbytes) & 15) == 0) {
+    const size_t nv = nbytes >> 4;
+    size_t i = lane;
+    for (; i + 32 < nv; i += 64) {
+      const uint4 a = ld_v4(src + (i << 4));
+      const uint4 b = ld_v4(src + ((i + 32) << 4));
+      st_v4(dst + (i << 4), a);
+      st_v4(dst + ((i + 32) << 4), b);
+    }
+    for (; i < nv; i += 32) st_v4(dst + (i << 4), ld_v4(src + (i << 4)));
+  } else {
+    for (size_t i = lane; i < nbytes; i += 32) dst[i] = src[i];
+  }
+}
+
+// Warp per token: ship the row (column shard tp_rank, or the full row to the
+// own group) once per host it hits, then publish per-slot metadata to the TP
+// peer on that host: recv_src[p] = u and the pair's (slot row, weight) list.
+template <class WT>
+__global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int n = v.n, m = v.m, k = v.k, E = v.E;
+  const int* ids = at<int>(v, v.rank, v.off.ids);
+  const WT* wts = at<WT>(v, v.rank, v.off.w);
+  const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
+  const int* upos = at<int>(v, v.rank, v.off.upos);
+  const size_t row_bytes = (size_t)v.h * v.elt;
+  int c0, c1;
+  col_shard(v.h, m, v.tp_rank, &c0, &c1);
+  const size_t sh_off = (size_t)c0 * v.elt, sh_bytes = (size_t)(c1 - c0) * v.elt;
+  for (long long t = gw; t < v.T; t += nwarps) {
+    const char* row = x + (size_t)t * row_bytes;
+    for (int d = 0; d < n; ++d) {
+      const int u = upos[t * n + d];
+      if (u < 0) continue;
+      if (d == v.group) {
+        copy_row(at<char>(v, v.rank, v.off.xbuf) + (size_t)u * row_bytes, row, row_bytes, lane);
+      } else {
+        for (int tt = 0; tt < m; ++tt)
+          copy_row(at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes + sh_off,
+                   row + sh_off, sh_bytes, lane);
+      }
+    }
+    // metadata: lane i carries slot i
+    int e = 0, d = -1;
+    if (lane < k) {
+      e = ids[t * k + lane];
+      d = home_of(e, n, E);
+    }
+    int idx = 0, cnt = 0;
+    for (int o = 0; o < k; ++o) {
+      const int oe = __shfl_sync(0xffffffffu, e, o);
+      const int od = __shfl_sync(0xffffffffu, d, o);
+      if (od == d) {
+        ++cnt;
+        if (oe < e) ++idx;
+      }
+    }
+    if (lane < k) {
+      const int u = upos[t * n + d];
+      const int p = slot_pos[t * k + lane];
+      const int dst = d * m + v.tp_rank;  // the TP peer that reads this metadata
+      if (p < v.cap) at<int>(v, dst, v.off.recv_src)[p] = u;
+      at<int>(v, dst, v.off.pair_p)[(size_t)u * v.KH + idx] = p;
+      at<WT>(v, dst, v.off.pair_w)[(size_t)u * v.KH + idx] = wts[t * k + lane];
+      if (idx == 0) at<int>(v, dst, v.off.pair_n)[u] = cnt;
+    }
+  }
+}
+
+// Host side: expert-major RECV rows from the deduplicated XBUF (local HBM).
+__global__ void __launch_bounds__(256) k_expand(DevView v) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int rows = at<int>(v, v.rank, v.off.host_rows)[v.group];
+  const int* src = at<int>(v, v.rank, v.off.recv_src);
+  const size_t row_bytes = (size_t)v.h * v.elt;
+  const char* xbuf = at<char>(v, v.rank, v.off.xbuf);
+  char* recv = at<char>(v, v.rank, v.off.recv);
+  for (long long p = gw; p < rows; p += nwarps)
+    copy_row(recv + p * row_bytes, xbuf + (size_t)src[p] * row_bytes, row_bytes, lane);
+}
+
+// z[u] = sum over the pair's slots (experts ascending) of w * partial[p].
+template <int DT>
+__global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  constexpr int V = Elt<DT>::V;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
+  const int* pn = at<int>(v, v.rank, v.off.pair_n);
+  const int* pp = at<int>(v, v.rank, v.off.pair_p);
+  const A* pw = at<A>(v, v.rank, v.off.pair_w);
+  const T* part = at<T>(v, v.rank, v.off.partial);
+  T* z = at<T>(v, v.rank, v.off.z);
+  const int h = v.h;
+  for (long long u = gw; u < pairs; u += nwarps) {
+    const int cnt = pn[u];
+    int prow[MX_KMAX];
+    A w[MX_KMAX];
+    for (int i = 0; i < cnt; ++i) {
+      prow[i] = pp[u * v.KH + i];
+      w[i] = pw[u * v.KH + i];
+    }
+    for (int c = lane * V; c < h; c += 32 * V) {
+      A acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = (A)0;
+      for (int i = 0; i < cnt; ++i) {
+        const uint4 raw = ld_v4(part + (size_t)prow[i] * h + c);
+        const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+      }
+      T out[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+      st_v4(z + (size_t)u * h + c, *reinterpret_cast<uint4*>(out));
+    }
+  }
+}
+
+// Owner (j, t): y[tok, cols t] = sum over hosts (j-1, ..., j) and TP ranks
+// (ascending) of z; then push the shard to every TP rank of the group.
+template <int DT>
+__global__ void __launch_bounds__(256) k_combine_token(DevView v) {
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  constexpr int V = Elt<DT>::V;
+  constexpr int HMAX = 8;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int n = v.n, m = v.m, h = v.h, j = v.group;
+  const int* upos = at<int>(v, v.rank, v.off.upos);
+  int c0, c1;
+  col_shard(h, m, v.tp_rank, &c0, &c1);
+  for (long long t = gw; t < v.T; t += nwarps) {
+    int hs[HMAX], us[HMAX], nh = 0;
+    for (int i = 1; i <= n; ++i) {
+      const int d = (j - i + n) % n;  // arrival order j-1, ..., j
+      const int u = upos[t * n + d];
+      if (u >= 0 && nh < HMAX) { hs[nh] = d; us[nh] = u; ++nh; }
+    }
+    for (int c = c0 + lane * V; c < c1; c += 32 * V) {
+      A acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = (A)0;
+      for (int tt = 0; tt < m; ++tt) {
+        uint4 raw[HMAX];
+#pragma unroll
+        for (int a = 0; a < HMAX; ++a)
+          if (a < nh) raw[a] = ld_v4(at<T>(v, hs[a] * m + tt, v.off.z) + (size_t)us[a] * h + c);
+#pragma unroll
+        for (int a = 0; a < HMAX; ++a)
+          if (a < nh) {
+            const T* pv = reinterpret_cast<const T*>(&raw[a]);
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
+          }
+      }
+      T out[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+      for (int tt = 0; tt < m; ++tt)
+        st_v4(at<T>(v, j * m + tt, v.off.y) + (size_t)t * h + c, *reinterpret_cast<uint4*>(out));
+    }
+  }
+}
+
+static int blocks_for(long long warps) {
+  long long b = (warps + 7) / 8;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)b;
+}
+
+static int check_vec(const DevView& v) {
+  int c0, c1;
+  col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
+  if (((size_t)c0 * v.elt) % 16 || ((size_t)(c1 - c0) * v.elt) % 16 || ((size_t)v.h * v.elt) % 16) {
+    set_error("wire TOKEN needs 16-byte aligned column shards (h*elt/m %% 16 == 0)");
+    return MX_ERR_UNSUPPORTED;
+  }
+  if (v.n > 8) { set_error("wire TOKEN supports up to 8 groups"); return MX_ERR_UNSUPPORTED; }
+  return MX_OK;
+}
+
+int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s) {
+  int rc = check_vec(v);
+  if (rc) return rc;
+  if (v.T == 0) return MX_OK;
+  if (v.elt == 8) k_dispatch_token<double><<<blocks_for(v.T), 256, 0, s>>>(v, static_cast<const char*>(x));
+  else k_dispatch_token<float><<<blocks_for(v.T), 256, 0, s>>>(v, static_cast<const char*>(x));
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+int launch_expand(const DevView& v, cudaStream_t s) {
+  k_expand<<<blocks_for(v.cap), 256, 0, s>>>(v);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+int launch_pair_reduce(const DevView& v, cudaStream_t s) {
+  const int g = blocks_for((long long)v.T * v.n);
+  switch (v.elt) {
+    case 8: k_pair_reduce<MX_F64><<<g, 256, 0, s>>>(v); break;
+    case 4: k_pair_reduce<MX_F32><<<g, 256, 0, s>>>(v); break;
+    default: k_pair_reduce<MX_BF16><<<g, 256, 0, s>>>(v);
+  }
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+int launch_combine_token(const DevView& v, cudaStream_t s) {
+  int rc = check_vec(v);
+  if (rc) return rc;
+  if (v.T == 0) return MX_OK;
+  const int g = blocks_for(v.T);
+  switch (v.elt) {
+    case 8: k_combine_token<MX_F64><<<g, 256, 0, s>>>(v); break;
+    case 4: k_combine_token<MX_F32><<<g, 256, 0, s>>>(v); break;
+    default: k_combine_token<MX_BF16><<<g, 256, 0, s>>>(v);
+  }
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // namespace mx

@@ -40,7 +40,7 @@ class MoELayer:
                  inter, experts: SwiGLUExperts | None = None, *, rank=None,
                  w13=None, w2=None, dtype=torch.bfloat16, renormalize=True,
                  capacity=None, expert_kind="swiglu", scales=None, biases=None,
-                 process_group=None):
+                 process_group=None, wire="slot"):
         self.n, self.m, self.W = n, m, n * m
         if rank is None:
             rank = dist.get_rank() if dist.is_initialized() else 0
@@ -53,7 +53,8 @@ class MoELayer:
                               top_k, dtype=dtype, expert_kind=expert_kind,
                               inter=inter, renormalize=renormalize,
                               capacity=capacity, emulate=False, rank=rank,
-                              process_group=process_group)
+                              process_group=process_group, wire=wire)
+        self.wire = wire
         if expert_kind == "swiglu":
             if w13 is None:
                 w13, w2 = experts.rank_shard(n, m, rank)
@@ -108,10 +109,17 @@ class MoELayer:
         p.layout(rank=r, stream=s); mark("layout")
         p.dispatch(x, rank=r, stream=s); mark("dispatch")
         p.barrier(stream=s); mark("barrier_dispatch")
+        tok = self.wire == "token"
+        if tok:
+            N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 3, sp), "expand")
+            mark("expand")
         N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 1, sp), "gemm1")
         mark("gemm1_swiglu")
         N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 2, sp), "gemm2")
         mark("gemm2")
+        if tok:
+            N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 4, sp), "pair_reduce")
+            mark("pair_reduce")
         p.barrier(stream=s); mark("barrier_partials")
         p.combine(rank=r, stream=s); mark("combine")
         p.barrier(stream=s); mark("barrier_out")
@@ -177,7 +185,8 @@ class MoELayer:
         mark("a2a_dispatch")
         N.check(lib.mx_baseline_dispatch_unpack(p._plan, r, C.c_void_p(recvbuf.data_ptr()),
                                                 sp), "unpack")
-        N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), 0, sp), "expert")
+        for stage in (1, 2):  # the GEMMs only (no wire-TOKEN expand/pre-reduce)
+            N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), stage, sp), "expert")
         mark("expert")
         back = torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=x.device)
         N.check(lib.mx_baseline_combine_pack(p._plan, r, C.c_void_p(back.data_ptr()),

@@ -86,6 +86,16 @@ def main():
     y_bl = layer.forward_baseline(xs, ls).clone()
     ys = gather_rows(y, world)
     ybs = gather_rows(y_bl, world)
+    layer.close()
+    # wire TOKEN (dedup dispatch + pre-reduced combine), eager and graph replay
+    layer = MoELayer(n, m, T, h, E, k, I, experts=ex, rank=rank, wire="token")
+    y_tok = layer.forward(xs, ls).clone()
+    run = layer.capture(xs, ls)
+    y_tok_g = run().clone()
+    torch.cuda.synchronize()
+    if not torch.equal(y_tok, y_tok_g):
+        failures.append("wire token: graph replay differs from eager")
+    yts = gather_rows(y_tok, world)
     if rank == 0:
         oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
                                ex.w_down.float().cpu().numpy())
@@ -96,9 +106,13 @@ def main():
             ref = y_ref[gg * T:(gg + 1) * T]
             e1 = orc.verify_metric(ys[r].float().cpu().numpy(), ref)
             e2 = orc.verify_metric(ybs[r].float().cpu().numpy(), ref)
-            print(f"rank {r}: fused err {e1:.3e}, nccl-baseline err {e2:.3e}", flush=True)
+            e3 = orc.verify_metric(yts[r].float().cpu().numpy(), ref)
+            print(f"rank {r}: fused err {e1:.3e}, nccl-baseline err {e2:.3e}, "
+                  f"token-wire err {e3:.3e}", flush=True)
             if e1 > 2e-2:
                 failures.append(f"swiglu fused rank {r}: err {e1:.3e}")
+            if e3 > 2e-2:
+                failures.append(f"swiglu token wire rank {r}: err {e3:.3e}")
             if e2 > 2e-2:
                 failures.append(f"swiglu baseline rank {r}: err {e2:.3e}")
     layer.close()

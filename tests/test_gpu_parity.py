@@ -322,3 +322,53 @@ def test_layer_graph_replay_matches_eager_and_oracle():
     y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
     assert orc.verify_metric(y2.float().cpu().numpy(), y_o) <= 2e-2
     layer.close()
+
+
+# ----------------------------------------------------------------- wire TOKEN
+@pytest.mark.parametrize("shape", [(1, 1), (2, 1), (2, 2), (4, 2), (2, 4), (8, 1), (4, 4)])
+def test_wire_token_f64_affine_emulated(shape):
+    """Dedup dispatch + pre-reduced combine: same outputs as the reference
+    layer up to f64 association (weights folded before the TP sum)."""
+    from paper_2601_08800_b200 import RouterSpec, _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    n, m = shape
+    T, h, E, k = 40, 64, 16, 4
+    rng = np.random.default_rng(n * 7 + m)
+    x = rng.standard_normal((n * T, h))
+    router = RouterSpec.random(n * T, E, k, seed=n + m)
+    ids, w = router.arrays()
+    sc, bi = np.arange(1, E + 1, dtype=np.float64), np.arange(E, dtype=np.float64)
+    plan = LayerPlan(n, m, T, h, E, k, dtype=torch.float64, wire="token")
+    sct, bit = torch.as_tensor(sc).cuda(), torch.as_tensor(bi).cuda()
+    params = N.ExpertParams(sct.data_ptr(), bit.data_ptr(), None, None)
+    y = torch.empty(n * T, h, dtype=torch.float64, device="cuda")
+    xt = torch.as_tensor(x).cuda()
+    plan.forward(xt, params, ids=torch.as_tensor(ids).cuda(), weights=torch.as_tensor(w).cuda(),
+                 y_out=y)
+    y_ref, _ = orc.run_fused_affine(n, m, x, ids, w, E, sc, bi)
+    assert orc.verify_metric(y.cpu().numpy(), y_ref) <= 1e-12
+    plan.close()
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (4, 2), (2, 4)])
+def test_wire_token_swiglu_emulated(shape):
+    from paper_2601_08800_b200 import SwiGLUExperts, _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    n, m = shape
+    T, h, E, k, I = 64, 256, 16, 4, 512
+    ex = SwiGLUExperts.random(E, h, I, seed=4)
+    w13, w2 = ex.stacked_shards(n, m)
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    x = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = torch.randn(n * T, E, device="cuda", generator=gen)
+    plan = LayerPlan(n, m, T, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu", inter=I,
+                     wire="token")
+    y = torch.empty(n * T, h, dtype=torch.bfloat16, device="cuda")
+    plan.forward(x, N.ExpertParams(None, None, w13.data_ptr(), w2.data_ptr()), logits=logits,
+                 y_out=y)
+    oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
+    assert orc.verify_metric(y.float().cpu().numpy(), y_o) <= 2e-2
+    plan.close()
