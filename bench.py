@@ -195,9 +195,10 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours
-def phase_model(S, cnt, n, m, group, tp, T):
+def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
     """Algorithmic bytes / flops per launch of every phase on this rank
-    (SURVEY.md §8(d)); S[j][d] = slots of group j hosted on group d."""
+    (SURVEY.md §8(d)); S[j][d] = slots of group j hosted on group d,
+    U[j][d] = tokens of group j hitting host d (wire TOKEN)."""
     It = INTER // m
     S_d = int(S[:, group].sum())             # rows this rank's GEMMs process
     remote_in = int(S[:, group].sum() - S[group, group])   # rows received over NVLink
@@ -221,6 +222,15 @@ def phase_model(S, cnt, n, m, group, tp, T):
         remote_pull = (slots * m - own_host_slots) * (H // m) * 2
         model["combine"] = {"bound": "nvlink",
                             "bytes": remote_pull + T * H * (m - 1) // m * 2}
+    if wire == "token" and U is not None:
+        U = np.asarray(U, dtype=np.int64)
+        remote_pairs = int(U[:, group].sum() - U[group, group])
+        model["dispatch"] = {"bound": "nvlink", "bytes": remote_pairs * hb}
+        model["expand"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
+        pairs_host = int(U[:, group].sum())
+        model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * hb + pairs_host * hb}
+        pull = (int(U[group].sum()) * m - int(U[group, group])) * (H // m) * 2
+        model["combine"] = {"bound": "nvlink", "bytes": pull + T * H * (m - 1) // m * 2}
     model["gemm1_swiglu"] = {"bound": "tensor", "flops": 2 * S_d * H * 2 * It}
     model["gemm2"] = {"bound": "tensor", "flops": 2 * S_d * It * H}
     return model
@@ -248,7 +258,8 @@ def run_ours(args):
     w13, w2 = ex.rank_shard(n, m, rank)
     del ex
     torch.cuda.empty_cache()
-    layer = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank)
+    wire = args.wire if args.wire != "auto" else ("token" if n > 1 else "slot")
+    layer = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank, wire=wire)
     g = torch.Generator(device="cuda").manual_seed(1000 + group)
     x = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
     logits = torch.randn(T, E, device="cuda", generator=g)
@@ -265,6 +276,7 @@ def run_ours(args):
     sync_all()
     S = layer.routing_counts()[1].astype(np.int64)
     cnt = layer.routing_counts()[0]
+    U = layer.pair_counts()
 
     # ---- timed region: K replays of the captured layer forward (one CUDA
     #      graph: every launch and device barrier), CUDA events around each
@@ -277,6 +289,7 @@ def run_ours(args):
         t_region0 = time.monotonic()
         for _ in range(args.steps):
             flush.fill_(1)
+            layer.plan.barrier()   # align ranks before the start event (launch skew)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -300,6 +313,7 @@ def run_ours(args):
     phase_times = {}
     for _ in range(args.steps):
         flush.fill_(1)
+        layer.plan.barrier()
         phased()
         torch.cuda.synchronize()
         for name, ms in phased.phase_ms():
@@ -314,6 +328,7 @@ def run_ours(args):
     e2e_ms = []
     for _ in range(args.steps):
         flush.fill_(1)
+        layer.plan.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -332,6 +347,30 @@ def run_ours(args):
     e2e_step = float(t.item()) / args.steps
     h2d = (x_h.numel() * 2 + l_h.numel() * 4) * world
     d2h = y_h.numel() * 2 * n
+
+    # ---- the reference's per-slot wire on the same config (N > 1)
+    slot_wire = None
+    if world > 1 and wire == "token" and not args.no_nccl:
+        alt = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank, wire="slot")
+        alt_run = alt.capture(x, logits)
+        ev = []
+        for _ in range(args.steps):
+            flush.fill_(1)
+            alt.plan.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            alt_run()
+            b.record(stream)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        st = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device="cuda")
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        slot_wire = {"ms_per_step": float(st.item()),
+                     "tokens_per_s": T_GLOBAL / (float(st.item()) / 1e3),
+                     "wire": "slot (the reference's one-row-per-slot A2A layout)"}
+        del alt_run
+        alt.close()
 
     # ---- NCCL AR + A2A baseline on the same config (N > 1)
     nccl = None
@@ -358,7 +397,7 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (this rank; rank 0 reports)
     pk, pk_kind = peaks()
-    model = phase_model(S, cnt, n, m, group, tp, T)
+    model = phase_model(S, cnt, n, m, group, tp, T, U, wire)
     avg = {k: float(np.mean(v)) for k, v in phase_times.items()}
     rooflines = {}
     for ph, spec in model.items():
@@ -394,7 +433,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(sample_tokens=args.cpu_sample)
 
-    launches_per_step = 8 + (4 if world > 1 else 0)  # route, scan, meta, slotpos, dispatch, gemm1, gemm2, combine (+4 barriers)
+    # gate, route, scan, meta, slotpos, dispatch, gemm1, gemm2, combine (+4 barriers;
+    # +expand, +pair_reduce for wire TOKEN)
+    launches_per_step = 9 + (4 if world > 1 else 0) + (2 if wire == "token" else 0)
     if rank == 0:
         line = {
             "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",
@@ -406,6 +447,7 @@ def run_ours(args):
                        "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP,
                        "global_tokens": T_GLOBAL, "groups_n": n, "tp_m": m,
                        "parallelism": f"TP{m}xEP{n}", "l2": "flushed (256 MiB write) between steps",
+                       "wire": wire,
                        "weights": "random init, seed 0"},
             "clocks": clk.summary(t_region0, t_region1),
             "e2e": {"value": T_GLOBAL / (e2e_step / 1e3), "unit": "tokens/s",
@@ -422,6 +464,8 @@ def run_ours(args):
         }
         if nccl is not None:
             line["nccl_baseline"] = nccl
+        if slot_wire is not None:
+            line["wire_slot"] = slot_wire
         print(json.dumps(line), flush=True)
     layer.close()
     if world > 1:
@@ -436,6 +480,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tp", type=int, default=None)
+    ap.add_argument("--wire", default="auto", choices=["auto", "slot", "token"],
+                    help="auto: token (dedup dispatch, pre-reduced combine) when n > 1")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=512)

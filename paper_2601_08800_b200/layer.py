@@ -135,6 +135,17 @@ class MoELayer:
         v = self.plan.rank_views(self.rank)
         return v["cnt_all"].cpu().numpy(), v["send"].cpu().numpy()
 
+    def pair_counts(self):
+        """U[j][d]: tokens of group j hitting host d (last forward), host."""
+        import numpy as _np
+        upos = self.plan.buffer(self.rank, N.MX_BUF_UPOS, torch.int32, (self.T, self.n))
+        mine = (upos >= 0).sum(0).to(torch.int64)
+        if dist.is_initialized() and self.W > 1:
+            allv = [torch.empty_like(mine) for _ in range(self.W)]
+            dist.all_gather(allv, mine)
+            return _np.stack([allv[j * self.m].cpu().numpy() for j in range(self.n)])
+        return mine.cpu().numpy()[None, :]
+
     # ------------------------------------------------------------ NCCL baseline
     def _groups(self):
         if self._ep_group is None:
