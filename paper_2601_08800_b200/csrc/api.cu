@@ -144,9 +144,9 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   const size_t U = tok ? T * n : 0;
   const size_t KH = kh_of(d);
   o.xbuf = take(U * h * elt);
-  o.recv_src = take(tok ? 4 * (size_t)cap : 0);
-  o.pair_p = take(4 * U * KH);
-  o.pair_w = take(wsz * U * KH);
+  o.recv_src = take(0);
+  o.pair_p = take(2 * wsz * U * KH);  // packed {row, weight} entries
+  o.pair_w = take(0);
   o.pair_n = take(4 * U);
   o.z = take(U * h * elt);
   o.total = p;

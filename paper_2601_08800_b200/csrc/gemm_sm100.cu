@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "mx_internal.cuh"
@@ -36,7 +37,8 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGING = 4 * 2 * 32 * 64;  // per epilogue warp: 2 x (32 rows x 64 B)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + STAGING;
 };
 
 // ------------------------------------------------------------ PTX wrappers
@@ -128,6 +130,42 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Stage one 32-row x 32-col bf16 chunk (64 B per row, thread = row) in the
+// SWIZZLE_64B layout the D tensor map expects (16 B chunk j of row r lives
+// at chunk j ^ ((r >> 1) & 3)), then one lane TMA-stores the 32x32 box.
+// Rows are complete boxes only; partial boxes use direct stores.
+__device__ __forceinline__ void stage_store_chunk(unsigned char* stg, const uint32_t (&p)[16],
+                                                  int lane, const CUtensorMap* map, int col,
+                                                  int row0) {
+  if (lane == 0) tma_store_wait_read1();  // this buffer's previous store has been read
+  __syncwarp();
+  unsigned char* rowp = stg + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t addr = smem_u32(rowp + ((j ^ ((lane >> 1) & 3)) << 4));
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(p[4 * j]),
+                 "r"(p[4 * j + 1]), "r"(p[4 * j + 2]), "r"(p[4 * j + 3])
+                 : "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) tma_store_2d(map, stg, col, row0);
+}
+
 struct Args {
   void* D;
   const int32_t* offs;
@@ -154,7 +192,8 @@ __device__ __forceinline__ void decode_tile(int t, const int* s_tstart, int G, i
 template <int BN, bool SWIGLU>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
-               const __grid_constant__ CUtensorMap map_b, Args args) {
+               const __grid_constant__ CUtensorMap map_b,
+               const __grid_constant__ CUtensorMap map_d, Args args) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -165,6 +204,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;  // [2]
   uint64_t* tempty = tfull + 2;         // [2]
+  unsigned char* staging = smem + C::STAGES * C::STAGE_BYTES + 1024;  // 1 KiB aligned
   __shared__ uint32_t s_tmem;
   __shared__ int s_tstart[MX_EMAX + 1];
   __shared__ int s_off[MX_EMAX];
@@ -199,6 +239,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
+    if (!args.out_f32) tma_prefetch(&map_d);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -276,6 +317,8 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
     // ===== epilogue: thread = accumulator row (TMEM lane)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = q * 32 + lane;
+    unsigned char* my_stage = staging + q * (2 * 32 * 64);
+    int buf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
@@ -285,6 +328,9 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       const int r_local = mb * BM + row_in_tile;
       const bool valid = r_local < cnt;
       const long long row = (long long)s_off[g] + r_local;
+      // the warp's 32 rows all belong to this group -> TMA box store
+      const bool full_box = !args.out_f32 && (mb * BM + q * 32 + 31) < cnt;
+      const int row0 = s_off[g] + mb * BM + q * 32;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -297,15 +343,18 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           tmem_ld32(tbase + c, gr);
           tmem_ld32(tbase + BN / 2 + c, ur);
           tmem_wait_ld();
-          if (valid) {
-            uint32_t packed[16];
+          uint32_t packed[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float a0 = silu(__uint_as_float(gr[2 * i])) * __uint_as_float(ur[2 * i]);
-              const float a1 = silu(__uint_as_float(gr[2 * i + 1])) * __uint_as_float(ur[2 * i + 1]);
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
-              packed[i] = *reinterpret_cast<uint32_t*>(&b2);
-            }
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = silu(__uint_as_float(gr[2 * i])) * __uint_as_float(ur[2 * i]);
+            const float a1 = silu(__uint_as_float(gr[2 * i + 1])) * __uint_as_float(ur[2 * i + 1]);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+            packed[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          if (full_box) {
+            stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * (BN / 2) + c, row0);
+            buf ^= 1;
+          } else if (valid) {
             uint4* dst = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -318,22 +367,27 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           uint32_t r[32];
           tmem_ld32(tbase + c, r);
           tmem_wait_ld();
-          if (valid) {
-            if (args.out_f32) {
+          if (args.out_f32) {
+            if (valid) {
               float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.D) + row * args.ldd +
                                                       nb * BN + c);
 #pragma unroll
               for (int i = 0; i < 8; ++i)
                 dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
                                      __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-            } else {
-              uint32_t packed[16];
+            }
+          } else {
+            uint32_t packed[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                __nv_bfloat162 b2 =
-                    __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-                packed[i] = *reinterpret_cast<uint32_t*>(&b2);
-              }
+            for (int i = 0; i < 16; ++i) {
+              __nv_bfloat162 b2 =
+                  __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+              packed[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            if (full_box) {
+              stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * BN + c, row0);
+              buf ^= 1;
+            } else if (valid) {
               uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.D) +
                                                     row * args.ldd + nb * BN + c);
 #pragma unroll
@@ -348,6 +402,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) tma_store_wait_all();
   }
 
   tc_fence_before();
@@ -374,15 +429,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const void* base, long long rows, int cols, int box_rows) {
+static int make_map(CUtensorMap* map, const void* base, long long rows, int cols, int box_rows,
+                    int box_cols = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return MX_ERR_CUDA; }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%d", (int)r, rows, cols);
@@ -402,8 +458,8 @@ static int sm_count() {
 }
 
 template <int BN, bool SWIGLU>
-static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, long long max_tiles,
-                  cudaStream_t s) {
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                  const Args& a, long long max_tiles, cudaStream_t s) {
   auto kern = k_grouped_gemm<BN, SWIGLU>;
   static bool attr = false;
   if (!attr) {
@@ -412,7 +468,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, l
   }
   long long grid = sm_count();
   if (max_tiles < grid) grid = max_tiles < 1 ? 1 : max_tiles;
-  kern<<<(int)grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ma, mb, a);
+  kern<<<(int)grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ma, mb, md, a);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -429,22 +485,27 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   if (out_dtype != MX_BF16 && out_dtype != MX_F32) { set_error("grouped_gemm: out dtype"); return MX_ERR_UNSUPPORTED; }
   if (M_cap < 1) return MX_OK;
   const int bn = (N % 256 == 0) ? 256 : 128;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, md;
+  memset(&md, 0, sizeof(md));
   int rc = make_map(&ma, A, M_cap, K, BM);
   if (rc) return rc;
   // B rows: every group's N rows (b_index may address any of them)
   long long b_rows = (long long)G * N;
   rc = make_map(&mb, B, b_rows, K, bn);
   if (rc) return rc;
+  if (out_dtype == MX_BF16) {  // 32x32 output boxes, 64 B swizzle (staged epilogue)
+    rc = make_map(&md, D, M_cap, swiglu ? N / 2 : N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
   Args a{};
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index;
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
   a.M_cap = M_cap;
   // upper bound on tiles (host does not know the per-group counts)
   const long long max_tiles = ((M_total + BM - 1) / BM + G) * (N / bn);
-  if (bn == 256) return swiglu ? launch<256, true>(ma, mb, a, max_tiles, s)
-                               : launch<256, false>(ma, mb, a, max_tiles, s);
-  return launch<128, false>(ma, mb, a, max_tiles, s);
+  if (bn == 256) return swiglu ? launch<256, true>(ma, mb, md, a, max_tiles, s)
+                               : launch<256, false>(ma, mb, md, a, max_tiles, s);
+  return launch<128, false>(ma, mb, md, a, max_tiles, s);
 }
 
 // Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.

@@ -17,6 +17,12 @@
 
 namespace mx {
 
+// One pair-list entry: expert-major row of the slot and its top-k weight,
+// written with a single remote store.
+template <class WT> struct PairEnt;
+template <> struct __align__(8) PairEnt<float> { int p; float w; };
+template <> struct __align__(16) PairEnt<double> { int p; int pad; double w; };
+
 __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbytes, int lane) {
   if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | nbytes) & 15) == 0) {
     const size_t nv = nbytes >> 4;
@@ -35,7 +41,7 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 
 // Warp per token: ship the row (column shard tp_rank, or the full row to the
 // own group) once per host it hits, then publish per-slot metadata to the TP
-// peer on that host: recv_src[p] = u and the pair's (slot row, weight) list.
+// peer on that host: the pair's packed (slot row, weight) list and its length.
 template <class WT>
 __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* __restrict__ x) {
   const int lane = threadIdx.x & 31;
@@ -82,61 +88,92 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
       const int u = upos[t * n + d];
       const int p = slot_pos[t * k + lane];
       const int dst = d * m + v.tp_rank;  // the TP peer that reads this metadata
-      if (p < v.cap) at<int>(v, dst, v.off.recv_src)[p] = u;
-      at<int>(v, dst, v.off.pair_p)[(size_t)u * v.KH + idx] = p;
-      at<WT>(v, dst, v.off.pair_w)[(size_t)u * v.KH + idx] = wts[t * k + lane];
+      PairEnt<WT> ent;
+      ent.p = p;
+      ent.w = wts[t * k + lane];
+      reinterpret_cast<PairEnt<WT>*>(at<char>(v, dst, v.off.pair_p))[(size_t)u * v.KH + idx] = ent;
       if (idx == 0) at<int>(v, dst, v.off.pair_n)[u] = cnt;
     }
   }
 }
 
-// Host side: expert-major RECV rows from the deduplicated XBUF (local HBM).
+// Host side: expert-major RECV rows from the deduplicated XBUF (local HBM),
+// warp per pair: each 512 B column chunk of the pair's row is loaded once and
+// stored to every slot row of the pair.
+template <class WT>
 __global__ void __launch_bounds__(256) k_expand(DevView v) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int rows = at<int>(v, v.rank, v.off.host_rows)[v.group];
-  const int* src = at<int>(v, v.rank, v.off.recv_src);
-  const size_t row_bytes = (size_t)v.h * v.elt;
-  const char* xbuf = at<char>(v, v.rank, v.off.xbuf);
-  char* recv = at<char>(v, v.rank, v.off.recv);
-  for (long long p = gw; p < rows; p += nwarps)
-    copy_row(recv + p * row_bytes, xbuf + (size_t)src[p] * row_bytes, row_bytes, lane);
-}
-
-// z[u] = sum over the pair's slots (experts ascending) of w * partial[p].
-template <int DT>
-__global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
-  using T = typename Elt<DT>::T;
-  using A = typename Elt<DT>::Acc;
-  constexpr int V = Elt<DT>::V;
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
-  const int* pp = at<int>(v, v.rank, v.off.pair_p);
-  const A* pw = at<A>(v, v.rank, v.off.pair_w);
+  const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
+  const size_t row_bytes = (size_t)v.h * v.elt;
+  const char* xbuf = at<char>(v, v.rank, v.off.xbuf);
+  char* recv = at<char>(v, v.rank, v.off.recv);
+  for (long long u = gw; u < pairs; u += nwarps) {
+    const int cnt = pn[u];
+    int rows[MX_KMAX];
+    for (int i = 0; i < cnt; ++i) rows[i] = pe[u * v.KH + i].p;
+    const char* src = xbuf + (size_t)u * row_bytes;
+    for (size_t o = (size_t)lane * 16; o < row_bytes; o += 512) {
+      const uint4 val = ld_v4(src + o);
+      for (int i = 0; i < cnt; ++i) st_v4(recv + (size_t)rows[i] * row_bytes + o, val);
+    }
+  }
+}
+
+// z[u] = sum over the pair's slots (experts ascending) of w * partial[p];
+// all slot loads of a column vector are issued before use (KU in flight).
+template <int DT, class WT>
+__global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  constexpr int V = Elt<DT>::V;
+  constexpr int KU = 8;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
+  const int* pn = at<int>(v, v.rank, v.off.pair_n);
+  const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
   const T* part = at<T>(v, v.rank, v.off.partial);
   T* z = at<T>(v, v.rank, v.off.z);
   const int h = v.h;
   for (long long u = gw; u < pairs; u += nwarps) {
     const int cnt = pn[u];
-    int prow[MX_KMAX];
-    A w[MX_KMAX];
-    for (int i = 0; i < cnt; ++i) {
-      prow[i] = pp[u * v.KH + i];
-      w[i] = pw[u * v.KH + i];
+    const T* rp[KU];
+    A w[KU];
+#pragma unroll
+    for (int i = 0; i < KU; ++i) {
+      const PairEnt<WT> e = pe[u * v.KH + (i < cnt ? i : 0)];
+      rp[i] = part + (size_t)e.p * h;
+      w[i] = (A)e.w;
     }
     for (int c = lane * V; c < h; c += 32 * V) {
       A acc[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) acc[q] = (A)0;
-      for (int i = 0; i < cnt; ++i) {
-        const uint4 raw = ld_v4(part + (size_t)prow[i] * h + c);
-        const T* pv = reinterpret_cast<const T*>(&raw);
+      if (cnt <= KU) {
+        uint4 raw[KU];
 #pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+        for (int i = 0; i < KU; ++i)
+          if (i < cnt) raw[i] = ld_v4(rp[i] + c);
+#pragma unroll
+        for (int i = 0; i < KU; ++i)
+          if (i < cnt) {
+            const T* pv = reinterpret_cast<const T*>(&raw[i]);
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+          }
+      } else {
+        for (int i = 0; i < cnt; ++i) {
+          const PairEnt<WT> e = pe[u * v.KH + i];
+          const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+          const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
+        }
       }
       T out[V];
 #pragma unroll
@@ -223,7 +260,8 @@ int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s) {
 }
 
 int launch_expand(const DevView& v, cudaStream_t s) {
-  k_expand<<<blocks_for(v.cap), 256, 0, s>>>(v);
+  if (v.elt == 8) k_expand<double><<<blocks_for((long long)v.T * v.n), 256, 0, s>>>(v);
+  else k_expand<float><<<blocks_for((long long)v.T * v.n), 256, 0, s>>>(v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -231,9 +269,9 @@ int launch_expand(const DevView& v, cudaStream_t s) {
 int launch_pair_reduce(const DevView& v, cudaStream_t s) {
   const int g = blocks_for((long long)v.T * v.n);
   switch (v.elt) {
-    case 8: k_pair_reduce<MX_F64><<<g, 256, 0, s>>>(v); break;
-    case 4: k_pair_reduce<MX_F32><<<g, 256, 0, s>>>(v); break;
-    default: k_pair_reduce<MX_BF16><<<g, 256, 0, s>>>(v);
+    case 8: k_pair_reduce<MX_F64, double><<<g, 256, 0, s>>>(v); break;
+    case 4: k_pair_reduce<MX_F32, float><<<g, 256, 0, s>>>(v); break;
+    default: k_pair_reduce<MX_BF16, float><<<g, 256, 0, s>>>(v);
   }
   MX_LAUNCH_CHECK();
   return MX_OK;
