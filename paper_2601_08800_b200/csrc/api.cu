@@ -144,7 +144,7 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   const size_t U = tok ? T * n : 0;
   const size_t KH = kh_of(d);
   o.xbuf = take(U * h * elt);
-  o.recv_src = take(0);
+  o.recv_src = take(4 * (size_t)cap);
   o.pair_p = take(2 * wsz * U * KH);  // packed {row, weight} entries
   o.pair_w = take(0);
   o.pair_n = take(4 * U);
@@ -173,6 +173,10 @@ struct mx_plan {
   long long cap = 0;
   Offsets off{};
   DevView base{};
+  // per rank: where GEMM1 gathers its A rows from (set by dispatch; cleared
+  // by the baseline's unpack, which materialises RECV instead)
+  const void* a_src[MX_MAXW] = {};
+  long long a_src_rows[MX_MAXW] = {};
 };
 
 static DevView view_for(const mx_plan* p, int r) {
@@ -180,7 +184,17 @@ static DevView view_for(const mx_plan* p, int r) {
   v.rank = r;
   v.group = r / p->d.tp;
   v.tp_rank = r % p->d.tp;
+  v.a_src = p->a_src[r];
+  v.a_src_rows = p->a_src_rows[r];
   return v;
+}
+
+// GEMM1 gathers token rows (TMA tile::gather4) instead of reading a
+// materialised expert-major copy: SwiGLU experts, and either one group
+// (rows straight from x) or the TOKEN wire (rows from the XBUF).
+static bool gathers(const mx_plan* p) {
+  return p->d.expert_kind == MX_EXPERT_SWIGLU &&
+         (p->d.wire == MX_WIRE_TOKEN || p->d.n_group == 1);
 }
 
 extern "C" {
@@ -454,8 +468,19 @@ int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream) {
   const size_t row = (size_t)p->d.hidden * elt_bytes(p->d.act_dtype);
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
-    rc = p->d.wire == MX_WIRE_TOKEN ? launch_dispatch_token(v, group_ptr(p, x, v.group, row), s)
-                                    : launch_dispatch(v, group_ptr(p, x, v.group, row), s);
+    const char* xg = group_ptr(p, x, v.group, row);
+    if (p->d.wire == MX_WIRE_TOKEN) {
+      rc = launch_dispatch_token(v, xg, s);
+      p->a_src[r] = gathers(p) ? static_cast<const void*>(p->comm->heap[r] + p->off.xbuf) : nullptr;
+      p->a_src_rows[r] = (long long)p->d.tokens * p->d.n_group;
+    } else if (gathers(p)) {
+      rc = launch_rowsrc_slot(v, s);  // n == 1: no row copies at all
+      p->a_src[r] = xg;
+      p->a_src_rows[r] = p->d.tokens;
+    } else {
+      rc = launch_dispatch(v, xg, s);
+      p->a_src[r] = nullptr;
+    }
     if (rc) return rc;
   }
   return MX_OK;
@@ -470,7 +495,11 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
     const bool tok = p->d.wire == MX_WIRE_TOKEN;
-    if (tok && (stage == 0 || stage == 3) && (rc = launch_expand(v, s))) return rc;
+    if (tok && (stage == 0 || stage == 3)) {
+      // gathered GEMM1 only needs the row table; otherwise expand into RECV
+      rc = v.a_src ? launch_rowsrc_token(v, s) : launch_expand(v, s);
+      if (rc) return rc;
+    }
     if (stage == 3 || stage == 4) {
       if (tok && stage == 4 && (rc = launch_pair_reduce(v, s))) return rc;
       continue;
@@ -563,6 +592,7 @@ int mx_baseline_dispatch_unpack(mx_plan* p, int rank, const void* recv, void* st
   int rc = ranks_for(p, rank, &it);
   if (rc) return rc;
   if (it.last - it.first != 1) { set_error("baseline helpers take one rank"); return MX_ERR_INVALID; }
+  p->a_src[it.first] = nullptr;  // RECV is materialised by the unpack
   return launch_baseline_dispatch_unpack(view_for(p, it.first), recv, static_cast<cudaStream_t>(stream));
 }
 

@@ -87,4 +87,28 @@ int launch_dispatch(const DevView& v, const void* x, cudaStream_t s) {
   return MX_OK;
 }
 
+// Single group (n == 1): every slot is local, so instead of copying rows into
+// the expert-major RECV the grouped GEMM gathers them straight from x; this
+// kernel only writes the row table recv_src[p] = token of slot p.
+__global__ void k_rowsrc_slot(DevView v) {
+  const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
+  int* src = at<int>(v, v.rank, v.off.recv_src);
+  const long long total = (long long)v.T * v.k;
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < total;
+       s += (long long)gridDim.x * blockDim.x) {
+    const int p = slot_pos[s];
+    if (p < v.cap) src[p] = (int)(s / v.k);
+  }
+}
+
+int launch_rowsrc_slot(const DevView& v, cudaStream_t s) {
+  const long long total = (long long)v.T * v.k;
+  if (total == 0) return MX_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_rowsrc_slot<<<(int)blocks, 256, 0, s>>>(v);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
 }  // namespace mx

@@ -71,6 +71,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 4 rows (row coordinates r0..r3, negative = zero fill) x 64 columns into
+// 512 contiguous bytes of smem, 128B swizzle applied by the TMA unit.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int col, int4 rows) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(rows.x),
+      "r"(rows.y), "r"(rows.z), "r"(rows.w)
+      : "memory");
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -168,6 +179,7 @@ __device__ __forceinline__ void stage_store_chunk(unsigned char* stg, const uint
 
 struct Args {
   void* D;
+  const int32_t* a_rows;  // GATHER: source row of every A row (row index table)
   const int32_t* offs;
   const int32_t* cnts;
   const int32_t* b_index;
@@ -189,7 +201,7 @@ __device__ __forceinline__ void decode_tile(int t, const int* s_tstart, int G, i
   *nb = r % nN;
 }
 
-template <int BN, bool SWIGLU>
+template <int BN, bool SWIGLU, bool GATHER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
                const __grid_constant__ CUtensorMap map_b,
@@ -265,7 +277,36 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   const int total_tiles = s_tstart[G];
 
   if (warp == 0) {
-    if (lane == 0) {
+    if constexpr (GATHER) {
+      // ===== TMA producer, gathered A: lane l brings rows 4l..4l+3 of the
+      // 128-row A tile with one tile::gather4 per k-block; lane 0 owns the
+      // barrier protocol and the B tile.
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int g, mb, nb;
+        decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+        const int bg = args.b_index ? args.b_index[g] : g;
+        const int b_row = bg * args.N + nb * BN;
+        const int r_local = mb * BM + 4 * lane;
+        const long long base = (long long)s_off[g] + r_local;
+        int4 rows;
+        rows.x = r_local + 0 < s_cnt[g] ? args.a_rows[base + 0] : -1;
+        rows.y = r_local + 1 < s_cnt[g] ? args.a_rows[base + 1] : -1;
+        rows.z = r_local + 2 < s_cnt[g] ? args.a_rows[base + 2] : -1;
+        rows.w = r_local + 3 < s_cnt[g] ? args.a_rows[base + 3] : -1;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * BK, b_row);
+          }
+          __syncwarp();
+          tma_gather4(sA + stage * C::A_BYTES + lane * 512, &map_a, &full[stage], kb * BK, rows);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else if (lane == 0) {
       // ===== TMA producer
       int stage = 0;
       uint32_t phase = 0;
@@ -457,10 +498,10 @@ static int sm_count() {
   return n;
 }
 
-template <int BN, bool SWIGLU>
+template <int BN, bool SWIGLU, bool GATHER>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                   const Args& a, long long max_tiles, cudaStream_t s) {
-  auto kern = k_grouped_gemm<BN, SWIGLU>;
+  auto kern = k_grouped_gemm<BN, SWIGLU, GATHER>;
   static bool attr = false;
   if (!attr) {
     MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
@@ -477,7 +518,8 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
 
 int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,
                  const int32_t* cnts, const int32_t* b_index, int G, long long M_total,
-                 long long M_cap, int N, int K, int swiglu, cudaStream_t s) {
+                 long long M_cap, int N, int K, int swiglu, cudaStream_t s,
+                 const int32_t* a_rows, long long a_src_rows) {
   using namespace gemm;
   if (G < 1 || G > MX_EMAX) { set_error("grouped_gemm: G=%d outside [1, %d]", G, MX_EMAX); return MX_ERR_UNSUPPORTED; }
   if (K % BK != 0 || N % 128 != 0) { set_error("grouped_gemm: K %% 64 and N %% 128 must be 0 (K=%d N=%d)", K, N); return MX_ERR_UNSUPPORTED; }
@@ -487,7 +529,9 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   const int bn = (N % 256 == 0) ? 256 : 128;
   CUtensorMap ma, mb, md;
   memset(&md, 0, sizeof(md));
-  int rc = make_map(&ma, A, M_cap, K, BM);
+  const bool gather = a_rows != nullptr;
+  // gathered A: box of 64 columns x 1 row, addressed 4 rows at a time
+  int rc = gather ? make_map(&ma, A, a_src_rows, K, 1) : make_map(&ma, A, M_cap, K, BM);
   if (rc) return rc;
   // B rows: every group's N rows (b_index may address any of them)
   long long b_rows = (long long)G * N;
@@ -498,14 +542,19 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
     if (rc) return rc;
   }
   Args a{};
-  a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index;
+  a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
   a.M_cap = M_cap;
   // upper bound on tiles (host does not know the per-group counts)
   const long long max_tiles = ((M_total + BM - 1) / BM + G) * (N / bn);
-  if (bn == 256) return swiglu ? launch<256, true>(ma, mb, md, a, max_tiles, s)
-                               : launch<256, false>(ma, mb, md, a, max_tiles, s);
-  return launch<128, false>(ma, mb, md, a, max_tiles, s);
+  if (gather) {
+    if (bn == 256) return swiglu ? launch<256, true, true>(ma, mb, md, a, max_tiles, s)
+                                 : launch<256, false, true>(ma, mb, md, a, max_tiles, s);
+    return launch<128, false, true>(ma, mb, md, a, max_tiles, s);
+  }
+  if (bn == 256) return swiglu ? launch<256, true, false>(ma, mb, md, a, max_tiles, s)
+                               : launch<256, false, false>(ma, mb, md, a, max_tiles, s);
+  return launch<128, false, false>(ma, mb, md, a, max_tiles, s);
 }
 
 // Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.
@@ -517,12 +566,16 @@ int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int 
   const int32_t* offs = at<int32_t>(v, v.rank, v.off.exp_off) + e0;
   const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
   if (stage != 2) {
-    int rc = grouped_gemm(at<char>(v, v.rank, v.off.recv), w13, at<char>(v, v.rank, v.off.act),
-                          MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, 2 * v.I_t, v.h, 1, s);
+    // GEMM1 A operand: gathered token rows (row table + source buffer) when
+    // the layout provides them, else the materialised expert-major RECV
+    const void* A = v.a_src ? v.a_src : at<char>(v, v.rank, v.off.recv);
+    const int32_t* rows = v.a_src ? at<int32_t>(v, v.rank, v.off.recv_src) : nullptr;
+    int rc = grouped_gemm(A, w13, at<char>(v, v.rank, v.off.act), MX_BF16, offs, cnts, nullptr, El,
+                          v.cap, v.cap, 2 * v.I_t, v.h, 1, s, rows, v.a_src_rows);
     if (rc || stage == 1) return rc;
   }
   return grouped_gemm(at<char>(v, v.rank, v.off.act), w2, at<char>(v, v.rank, v.off.partial),
-                      MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s);
+                      MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s, nullptr, 0);
 }
 
 }  // namespace mx

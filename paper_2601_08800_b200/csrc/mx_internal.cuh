@@ -62,7 +62,7 @@ struct Offsets {
   size_t tok_pair_rank;  // int32 [T][n] rank among chunk tokens hitting d (-1: none)
   size_t upos;        // int32 [T][n]  row of (token, d) in d's xbuf (-1: none)
   size_t xbuf;        // act [T*n][h]  deduplicated rows (peers write)
-  size_t recv_src;    // int32 [cap]   xbuf row of every expert-major row (peers write)
+  size_t recv_src;    // int32 [cap]   source row (token / xbuf pair) of every expert-major row
   size_t pair_p;      // int32 [T*n][KH] slot rows of a pair (peers write)
   size_t pair_w;      // AccT [T*n][KH]  slot weights of a pair (peers write)
   size_t pair_n;      // int32 [T*n]     slots of a pair (peers write)
@@ -79,6 +79,8 @@ struct DevView {
   int renorm;
   int wire;           // mx_wire
   int KH;             // max slots of one token on one host
+  const void* a_src;  // GEMM1 gathers A rows from here (x or XBUF), nullptr: RECV
+  long long a_src_rows;
   long long cap;
   Offsets off;
   char* heap[MX_MAXW];
@@ -181,6 +183,8 @@ int launch_baseline_combine_unpack(const DevView& v, const void* recv, void* y,
 int grouped_gemm(const void* A, const void* B, void* D, int out_dtype,
                  const int32_t* offs, const int32_t* cnts, const int32_t* b_index,
                  int G, long long M_total, long long M_cap, int N, int K, int swiglu,
-                 cudaStream_t s);
+                 cudaStream_t s, const int32_t* a_rows = nullptr, long long a_src_rows = 0);
+int launch_rowsrc_slot(const DevView& v, cudaStream_t s);
+int launch_rowsrc_token(const DevView& v, cudaStream_t s);
 
 }  // namespace mx

@@ -231,6 +231,23 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
   }
 }
 
+// Gathered GEMM1 (SwiGLU): the row table replaces the expansion copy --
+// recv_src[p] = u for every slot row p of pair u.
+template <class WT>
+__global__ void k_rowsrc_token(DevView v) {
+  const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
+  const int* pn = at<int>(v, v.rank, v.off.pair_n);
+  const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
+  int* src = at<int>(v, v.rank, v.off.recv_src);
+  const long long total = (long long)pairs * v.KH;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long u = q / v.KH;
+    const int i = (int)(q % v.KH);
+    if (i < pn[u]) src[pe[q].p] = (int)u;
+  }
+}
+
 static int blocks_for(long long warps) {
   long long b = (warps + 7) / 8;
   if (b < 1) b = 1;
@@ -262,6 +279,16 @@ int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s) {
 int launch_expand(const DevView& v, cudaStream_t s) {
   if (v.elt == 8) k_expand<double><<<blocks_for((long long)v.T * v.n), 256, 0, s>>>(v);
   else k_expand<float><<<blocks_for((long long)v.T * v.n), 256, 0, s>>>(v);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
+  long long blocks = ((long long)v.T * v.n * v.KH + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (v.elt == 8) k_rowsrc_token<double><<<(int)blocks, 256, 0, s>>>(v);
+  else k_rowsrc_token<float><<<(int)blocks, 256, 0, s>>>(v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
