@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary (include/mixserve_b200.h): symmetric
 // heap communicator, layer plan, phase sequencing and the device barrier.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -192,8 +193,15 @@ static DevView view_for(const mx_plan* p, int r) {
 // GEMM1 gathers token rows (TMA tile::gather4) instead of reading a
 // materialised expert-major copy: SwiGLU experts, and either one group
 // (rows straight from x) or the TOKEN wire (rows from the XBUF).
+// Measured on B200 (round 1): 32 gather4 ops per k-block throttle the TMA
+// producer -- GEMM1 964 us vs 374 us with the copy -- so it is opt-in
+// (MX_GATHER=1) until the producer is rebuilt on LDGSTS.
 static bool gathers(const mx_plan* p) {
-  return p->d.expert_kind == MX_EXPERT_SWIGLU &&
+  static const bool enabled = [] {
+    const char* e = getenv("MX_GATHER");
+    return e && e[0] == '1';
+  }();
+  return enabled && p->d.expert_kind == MX_EXPERT_SWIGLU &&
          (p->d.wire == MX_WIRE_TOKEN || p->d.n_group == 1);
 }
 
