@@ -265,118 +265,123 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
 }
 
 
-// Offsets of the layout from the gathered [n][E] count matrix (one CTA).
-__global__ void __launch_bounds__(1024) k_layout_meta(DevView v) {
-  const int n = v.n, E = v.E;
+// Layout in one launch: every CTA rebuilds the offset tables it needs from
+// the gathered [n][E] count matrix in shared memory (a few KB), CTA 0 also
+// publishes the global tables (exp_off/exp_cnt/grp_off/send/...) for later kernels;
+// then the grid writes every slot's expert-major row and token-major index
+// and every (token, host) pair row.
+__global__ void __launch_bounds__(512) k_layout(DevView v) {
+  extern __shared__ int sm[];
+  const int n = v.n, E = v.E, k = v.k, j = v.group;
+  int* s_cnt = sm;                   // [n][E]
+  int* s_exp_off = s_cnt + n * E;    // [E]
+  int* s_grp_off = s_exp_off + E;    // [E] rows of groups < j, per expert
+  int* s_send = s_grp_off + E;       // [n][n]
+  int* s_tm = s_send + n * n;        // [n]  tm_off[j][d]
+  int* s_po = s_tm + n;              // [n]  poff[j][d]
+  int* s_part = s_po + n;            // [blockDim] scan partials
   const int* cnt = at<int>(v, v.rank, v.off.cnt_all);
-  int* exp_off = at<int>(v, v.rank, v.off.exp_off);
-  int* exp_cnt = at<int>(v, v.rank, v.off.exp_cnt);
-  int* grp_off = at<int>(v, v.rank, v.off.grp_off);
-  int* send = at<int>(v, v.rank, v.off.send);
-  int* tm_off = at<int>(v, v.rank, v.off.tm_off);
-  int* host_rows = at<int>(v, v.rank, v.off.host_rows);
-  int* err = at<int>(v, v.rank, v.off.err);
-  __shared__ int s_scan[MX_EMAX];
-  __shared__ int s_tot[MX_EMAX];
-  __shared__ int s_send[MX_NMAX * MX_NMAX];
-  const int e = threadIdx.x;
-  int tot = 0;
-  if (e < E) {
-    for (int j = 0; j < n; ++j) {
-      grp_off[j * E + e] = tot;  // rows of groups j' < j for expert e
-      tot += cnt[j * E + e];
-    }
-    exp_cnt[e] = tot;
-  }
-  s_tot[e] = tot;
-  s_scan[e] = tot;
+  const int* ucnt = at<int>(v, v.rank, v.off.ucnt_all);
+  const bool pub = blockIdx.x == 0;
+  for (int i = threadIdx.x; i < n * E; i += blockDim.x) s_cnt[i] = cnt[i];
   __syncthreads();
-  for (int o = 1; o < MX_EMAX; o <<= 1) {
-    const int y = (e >= o) ? s_scan[e - o] : 0;
-    __syncthreads();
-    s_scan[e] += y;
-    __syncthreads();
+  // per-expert totals, own-group offsets, host-segmented exclusive scan
+  const int per = (E + blockDim.x - 1) / blockDim.x;
+  const int e_lo = threadIdx.x * per, e_hi = min(E, e_lo + per);
+  int run = 0;
+  for (int e = e_lo; e < e_hi; ++e) {
+    int tot = 0, mine = 0;
+    for (int g = 0; g < n; ++g) {
+      if (g == j) mine = tot;
+      if (pub) at<int>(v, v.rank, v.off.grp_off)[g * E + e] = tot;
+      tot += s_cnt[g * E + e];
+    }
+    s_grp_off[e] = mine;
+    s_exp_off[e] = tot;  // holds totals until the scan below
+    if (pub) at<int>(v, v.rank, v.off.exp_cnt)[e] = tot;
+    run += tot;
   }
-  if (e < E) {
-    const int f = first_expert(home_of(e, n, E), n, E);
-    exp_off[e] = (s_scan[e] - tot) - (s_scan[f] - s_tot[f]);
+  s_part[threadIdx.x] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int t = 0; t < (int)blockDim.x; ++t) { const int x = s_part[t]; s_part[t] = acc; acc += x; }
   }
-  // S[j][d]: slots of group j's tokens hosted on group d
+  __syncthreads();
+  run = s_part[threadIdx.x];
+  for (int e = e_lo; e < e_hi; ++e) {  // global exclusive prefix of totals
+    const int tot = s_exp_off[e];
+    s_exp_off[e] = run;
+    run += tot;
+  }
+  __syncthreads();
+  // host-segmented: subtract the prefix at the first expert of each host
+  int* tmp = s_part;  // reuse: host segment bases (n <= blockDim)
+  for (int d = threadIdx.x; d < n; d += blockDim.x) tmp[d] = s_exp_off[first_expert(d, n, E)];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    s_exp_off[e] -= tmp[home_of(e, n, E)];
+  }
+  __syncthreads();
+  if (pub)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) at<int>(v, v.rank, v.off.exp_off)[e] = s_exp_off[e];
+  // send counts, token-major offsets, pair offsets
   for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
-    const int j = jd / n, d = jd % n;
+    const int g = jd / n, d = jd % n;
     const int e0 = first_expert(d, n, E), e1 = first_expert(d + 1, n, E);
-    int s = 0;
-    for (int x = e0; x < e1; ++x) s += cnt[j * E + x];
-    s_send[jd] = s;
-    send[jd] = s;
+    int sum = 0;
+    for (int x = e0; x < e1; ++x) sum += s_cnt[g * E + x];
+    s_send[jd] = sum;
+    if (pub) at<int>(v, v.rank, v.off.send)[jd] = sum;
   }
   __syncthreads();
   for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
-    const int j = jd / n, d = jd % n;
-    int s = 0;
-    for (int j2 = 0; j2 < j; ++j2) s += s_send[j2 * n + d];
-    tm_off[jd] = s;
-  }
-  {
-    const int* ucnt = at<int>(v, v.rank, v.off.ucnt_all);
-    int* poff = at<int>(v, v.rank, v.off.poff);
-    int* hp = at<int>(v, v.rank, v.off.host_pairs);
-    for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
-      const int j = jd / n, d = jd % n;
-      int s = 0;
-      for (int j2 = 0; j2 < j; ++j2) s += ucnt[j2 * n + d];
-      poff[jd] = s;
-      if (j == n - 1) hp[d] = s + ucnt[jd];
+    const int g = jd / n, d = jd % n;
+    int tm = 0, po = 0;
+    for (int g2 = 0; g2 < g; ++g2) { tm += s_send[g2 * n + d]; po += ucnt[g2 * n + d]; }
+    if (g == j) { s_tm[d] = tm; s_po[d] = po; }
+    if (pub) {
+      at<int>(v, v.rank, v.off.tm_off)[jd] = tm;
+      at<int>(v, v.rank, v.off.poff)[jd] = po;
+      if (g == n - 1) {
+        at<int>(v, v.rank, v.off.host_pairs)[d] = po + ucnt[jd];
+        const int rows = tm + s_send[jd];
+        at<int>(v, v.rank, v.off.host_rows)[d] = rows;
+        if ((long long)rows > v.cap) atomicMax(at<int>(v, v.rank, v.off.err) + 0, rows);
+      }
     }
   }
-  for (int d = threadIdx.x; d < n; d += blockDim.x) {
-    int s = 0;
-    for (int j = 0; j < n; ++j) s += s_send[j * n + d];
-    host_rows[d] = s;
-    if ((long long)s > v.cap) atomicMax(err + 0, s);  // CapacityError (sim:346-351)
-  }
-}
-
-// Final slot positions: expert-major row in the host's RECV buffer and the
-// index in the host's token-major routing table.
-__global__ void k_slotpos(DevView v) {
-  const int n = v.n, E = v.E, k = v.k;
+  __syncthreads();
+  // slot positions
   const int* ids = at<int>(v, v.rank, v.off.ids);
   const int* slot_rank = at<int>(v, v.rank, v.off.slot_rank);
   const int* slot_tmr = at<int>(v, v.rank, v.off.slot_tmr);
   const int* chunk_hist = at<int>(v, v.rank, v.off.chunk_hist);
   const int* chunk_host = at<int>(v, v.rank, v.off.chunk_host);
-  const int* exp_off = at<int>(v, v.rank, v.off.exp_off);
-  const int* grp_off = at<int>(v, v.rank, v.off.grp_off);
-  const int* tm_off = at<int>(v, v.rank, v.off.tm_off);
   int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
   int* slot_tm = at<int>(v, v.rank, v.off.slot_tm);
   int* err = at<int>(v, v.rank, v.off.err);
   const long long total = (long long)v.T * k;
-  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < total;
-       s += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(s / k);
-    const int e = ids[s];
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(q / k);
+    const int e = ids[q];
     const int d = home_of(e, n, E);
     const int c = t / MX_CHUNK;
-    const long long pos = (long long)exp_off[e] + grp_off[v.group * E + e] +
-                          chunk_hist[e * v.C + c] + slot_rank[s];
-    const int tm = tm_off[v.group * n + d] + chunk_host[d * v.C + c] + slot_tmr[s];
+    const long long pos = (long long)s_exp_off[e] + s_grp_off[e] + chunk_hist[e * v.C + c] + slot_rank[q];
     if (pos >= v.cap) atomicOr(err + 3, 1);
-    slot_pos[s] = (int)pos;
-    slot_tm[s] = tm;
+    slot_pos[q] = (int)pos;
+    slot_tm[q] = s_tm[d] + chunk_host[d * v.C + c] + slot_tmr[q];
   }
-  // (token, host) pair rows in the host's deduplicated buffer
   const int* tpr = at<int>(v, v.rank, v.off.tok_pair_rank);
   const int* chunk_pair = at<int>(v, v.rank, v.off.chunk_pair);
-  const int* poff = at<int>(v, v.rank, v.off.poff);
   int* upos = at<int>(v, v.rank, v.off.upos);
   const long long tn = (long long)v.T * n;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < tn;
        q += (long long)gridDim.x * blockDim.x) {
     const int t = (int)(q / n), d = (int)(q % n);
     const int r = tpr[q];
-    upos[q] = r < 0 ? -1 : poff[v.group * n + d] + chunk_pair[d * v.C + t / MX_CHUNK] + r;
+    upos[q] = r < 0 ? -1 : s_po[d] + chunk_pair[d * v.C + t / MX_CHUNK] + r;
   }
 }
 
@@ -421,14 +426,19 @@ int launch_route(const DevView& v, const float* logits, const int32_t* ids,
 }
 
 int launch_layout(const DevView& v, cudaStream_t s) {
-  k_layout_meta<<<1, 1024, 0, s>>>(v);
-  MX_LAUNCH_CHECK();
-  const long long total = (long long)v.T * v.k;
-  if (total > 0) {
-    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    k_slotpos<<<blocks, 256, 0, s>>>(v);
-    MX_LAUNCH_CHECK();
+  const size_t smem = ((size_t)v.n * v.E + 2 * v.E + (size_t)v.n * v.n + 2 * v.n + 512) * 4;
+  static bool attr = false;
+  if (!attr) {
+    MX_CUDA(cudaFuncSetAttribute(k_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
   }
+  if (smem > 200 * 1024) { set_error("layout tables exceed shared memory (n*E too large)"); return MX_ERR_UNSUPPORTED; }
+  const long long work = (long long)v.T * (v.k > v.n ? v.k : v.n);
+  long long blocks = (work + 511) / 512;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 2) blocks = 148 * 2;
+  k_layout<<<(int)blocks, 512, smem, s>>>(v);
+  MX_LAUNCH_CHECK();
   return MX_OK;
 }
 
