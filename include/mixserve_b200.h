@@ -214,6 +214,19 @@ MX_API int mx_grouped_gemm(const void* A, const void* B, void* D, int out_dtype,
                     const int32_t* offs, const int32_t* cnts, int G,
                     long long M_total, int N, int K, int swiglu, void* stream);
 
+/* fp8 (e4m3) expert path (BASELINE config C).  Rows carry their fp32
+ * scale: row r = cols e4m3 bytes, then the scale at byte `cols`; stride
+ * ld >= cols + 16 (16 B aligned).  scale = amax/448, RNE, saturating.    */
+MX_API int mx_quant_rows_e4m3(const void* src_bf16, long long lds_elems, void* dst,
+                              long long ldd_bytes, long long rows, int cols, void* stream);
+/* e4m3 grouped GEMM: A rows as above (lda bytes), B [G, N, K] e4m3 with
+ * b_scales [G, N] fp32 per output channel, D bf16 [M, N] (or [M, N/2]
+ * with the SwiGLU epilogue); f32 accumulation on tcgen05 kind::f8f6f4.   */
+MX_API int mx_grouped_gemm_fp8(const void* A, long long lda, const void* B,
+                               const float* b_scales, void* D, const int32_t* offs,
+                               const int32_t* cnts, int G, long long M_total, int N, int K,
+                               int swiglu, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

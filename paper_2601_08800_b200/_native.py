@@ -81,6 +81,8 @@ SIGNATURES = {
     "mx_dense_moe": [I, I, I, I, I, I, I, VP, VP, VP, VP, VP, VP, VP, VP,
                      VP, VP],
     "mx_grouped_gemm": [VP, VP, VP, I, VP, VP, I, LL, I, I, I, VP],
+    "mx_quant_rows_e4m3": [VP, LL, VP, LL, LL, I, VP],
+    "mx_grouped_gemm_fp8": [VP, LL, VP, VP, VP, VP, VP, I, LL, I, I, I, VP],
 }
 
 _lib = None

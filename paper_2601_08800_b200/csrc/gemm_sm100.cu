@@ -27,14 +27,15 @@ namespace mx {
 namespace gemm {
 
 constexpr int BM = 128;
-constexpr int BK = 64;  // 64 bf16 = 128 B rows: one SWIZZLE_128B atom wide
+constexpr int BK = 64;   // bf16 elements per k-block: 128 B rows, one SWIZZLE_128B atom wide
+constexpr int BKB = 128; // bytes per k-block row (64 bf16 or 128 e4m3)
 constexpr int NUM_THREADS = 256;
 
 template <int BN>
 struct Cfg {
   static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int A_BYTES = BM * BKB;
+  static constexpr int B_BYTES = BN * BKB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
   static constexpr int STAGING = 4 * 2 * 32 * 64;  // per epilogue warp: 2 x (32 rows x 64 B)
@@ -102,6 +103,19 @@ __device__ __forceinline__ constexpr uint32_t idesc_bf16() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
          ((uint32_t)(BM >> 4) << 24);
 }
+// kind::f8f6f4 with A = B = E4M3 (format code 0), D f32.
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t idesc_e4m3() {
+  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_e4m3(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -140,6 +154,18 @@ __device__ __forceinline__ void tmem_wait_ld() {
 }
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// FP8 dequantisation of 32 accumulator columns: v *= row_scale * col_scale[j]
+__device__ __forceinline__ void scale_cols(uint32_t (&r)[32], float sa, const float* __restrict__ sb) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(sb) + i);
+    r[4 * i + 0] = __float_as_uint(__uint_as_float(r[4 * i + 0]) * sa * b.x);
+    r[4 * i + 1] = __float_as_uint(__uint_as_float(r[4 * i + 1]) * sa * b.y);
+    r[4 * i + 2] = __float_as_uint(__uint_as_float(r[4 * i + 2]) * sa * b.z);
+    r[4 * i + 3] = __float_as_uint(__uint_as_float(r[4 * i + 3]) * sa * b.w);
+  }
+}
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -180,6 +206,9 @@ __device__ __forceinline__ void stage_store_chunk(unsigned char* stg, const uint
 struct Args {
   void* D;
   const int32_t* a_rows;  // GATHER: source row of every A row (row index table)
+  const char* a_base;     // FP8: A rows (lda bytes each), fp32 row scale at byte K
+  long long lda;          // FP8: A row stride in bytes
+  const float* b_scales;  // FP8: per-B-row (output channel) scales, [G*N]
   const int32_t* offs;
   const int32_t* cnts;
   const int32_t* b_index;
@@ -201,7 +230,7 @@ __device__ __forceinline__ void decode_tile(int t, const int* s_tstart, int G, i
   *nb = r % nN;
 }
 
-template <int BN, bool SWIGLU, bool GATHER>
+template <int BN, bool SWIGLU, bool GATHER, bool FP8>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
                const __grid_constant__ CUtensorMap map_b,
@@ -223,7 +252,8 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   __shared__ int s_cnt[MX_EMAX];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = args.G, nN = args.N / BN, kblocks = args.K / BK;
+  constexpr int KE = FP8 ? 128 : 64;  // elements per k-block (128 B)
+  const int G = args.G, nN = args.N / BN, kblocks = args.K / KE;
 
   // group offsets/counts -> smem (parallel loads), then the per-group tile
   // prefix by one warp-scan pass (G <= MX_EMAX); no per-tile global reads
@@ -299,10 +329,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           if (lane == 0) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * BK, b_row);
+            tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
           }
           __syncwarp();
-          tma_gather4(sA + stage * C::A_BYTES + lane * 512, &map_a, &full[stage], kb * BK, rows);
+          tma_gather4(sA + stage * C::A_BYTES + lane * 512, &map_a, &full[stage], kb * KE, rows);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -319,8 +349,8 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * BK, a_row);
-          tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * BK, b_row);
+          tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * KE, a_row);
+          tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -328,7 +358,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer (single thread)
-      constexpr uint32_t idesc = idesc_bf16<BN>();
+      constexpr uint32_t idesc = FP8 ? idesc_e4m3<BN>() : idesc_bf16<BN>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -343,9 +373,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // +32 B per K=16 step inside the 128 B swizzle atom (>>4 -> +2)
-            mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < 4; ++kk) {
+            // +32 B per MMA (K=16 bf16 / K=32 e4m3) inside the 128 B swizzle atom (>>4 -> +2)
+            if constexpr (FP8) mma_e4m3(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+            else mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
           }
           mma_commit(&empty[stage]);  // frees the smem slot when the MMAs retire
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -372,6 +403,13 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       // the warp's 32 rows all belong to this group -> TMA box store
       const bool full_box = !args.out_f32 && (mb * BM + q * 32 + 31) < cnt;
       const int row0 = s_off[g] + mb * BM + q * 32;
+      // FP8: per-row activation scale (row tail) and the group's weight scales
+      float sa = 1.f;
+      int bg = g;
+      if constexpr (FP8) {
+        bg = args.b_index ? args.b_index[g] : g;
+        if (valid) sa = *reinterpret_cast<const float*>(args.a_base + row * args.lda + args.K);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -384,6 +422,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           tmem_ld32(tbase + c, gr);
           tmem_ld32(tbase + BN / 2 + c, ur);
           tmem_wait_ld();
+          if constexpr (FP8) {
+            scale_cols(gr, sa, args.b_scales + (size_t)bg * args.N + nb * BN + c);
+            scale_cols(ur, sa, args.b_scales + (size_t)bg * args.N + nb * BN + BN / 2 + c);
+          }
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -408,6 +450,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           uint32_t r[32];
           tmem_ld32(tbase + c, r);
           tmem_wait_ld();
+          if constexpr (FP8) scale_cols(r, sa, args.b_scales + (size_t)bg * args.N + nb * BN + c);
           if (args.out_f32) {
             if (valid) {
               float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.D) + row * args.ldd +
@@ -471,14 +514,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 static int make_map(CUtensorMap* map, const void* base, long long rows, int cols, int box_rows,
-                    int box_cols = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                    int box_cols = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                    bool fp8 = false, long long row_bytes = 0) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return MX_ERR_CUDA; }
+  const int esz = fp8 ? 1 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)(row_bytes ? row_bytes : (long long)cols * esz)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = enc(map, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -498,10 +544,10 @@ static int sm_count() {
   return n;
 }
 
-template <int BN, bool SWIGLU, bool GATHER>
+template <int BN, bool SWIGLU, bool GATHER, bool FP8 = false>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                   const Args& a, long long max_tiles, cudaStream_t s) {
-  auto kern = k_grouped_gemm<BN, SWIGLU, GATHER>;
+  auto kern = k_grouped_gemm<BN, SWIGLU, GATHER, FP8>;
   static bool attr = false;
   if (!attr) {
     MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
@@ -555,6 +601,35 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   if (bn == 256) return swiglu ? launch<256, true, false>(ma, mb, md, a, max_tiles, s)
                                : launch<256, false, false>(ma, mb, md, a, max_tiles, s);
   return launch<128, false, false>(ma, mb, md, a, max_tiles, s);
+}
+
+// e4m3 x e4m3 -> f32 grouped GEMM with per-row activation scales (fp32 at
+// byte K of every A row, rows lda bytes apart) and per-output-channel weight
+// scales; D = bf16 (optionally SwiGLU).  The dequantised product equals
+// sum_k (qa*sa) (qb*sb) exactly as the CPU replica computes it.
+int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b_scales, void* D,
+                     const int32_t* offs, const int32_t* cnts, const int32_t* b_index, int G,
+                     long long M_total, long long M_cap, int N, int K, int swiglu, cudaStream_t s) {
+  using namespace gemm;
+  if (G < 1 || G > MX_EMAX) { set_error("grouped_gemm_fp8: G=%d outside [1, %d]", G, MX_EMAX); return MX_ERR_UNSUPPORTED; }
+  if (K % 128 != 0 || N % 256 != 0) { set_error("grouped_gemm_fp8: K %% 128 and N %% 256 must be 0 (K=%d N=%d)", K, N); return MX_ERR_UNSUPPORTED; }
+  if (lda < K + 4 || lda % 16 != 0) { set_error("grouped_gemm_fp8: lda must hold K bytes + fp32 scale, 16 B aligned"); return MX_ERR_UNSUPPORTED; }
+  if (M_cap < 1) return MX_OK;
+  CUtensorMap ma, mb, md;
+  int rc = make_map(&ma, A, M_cap, K, BM, 128, CU_TENSOR_MAP_SWIZZLE_128B, true, lda);
+  if (rc) return rc;
+  rc = make_map(&mb, B, (long long)G * N, K, 256, 128, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  if (rc) return rc;
+  rc = make_map(&md, D, M_cap, swiglu ? N / 2 : N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  Args a{};
+  a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index;
+  a.a_base = static_cast<const char*>(A); a.lda = lda; a.b_scales = b_scales;
+  a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = 0;
+  a.M_cap = M_cap;
+  const long long max_tiles = ((M_total + BM - 1) / BM + G) * (N / 256);
+  return swiglu ? launch<256, true, false, true>(ma, mb, md, a, max_tiles, s)
+                : launch<256, false, false, true>(ma, mb, md, a, max_tiles, s);
 }
 
 // Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.

@@ -184,6 +184,11 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype,
                  const int32_t* offs, const int32_t* cnts, const int32_t* b_index,
                  int G, long long M_total, long long M_cap, int N, int K, int swiglu,
                  cudaStream_t s, const int32_t* a_rows = nullptr, long long a_src_rows = 0);
+int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b_scales, void* D,
+                     const int32_t* offs, const int32_t* cnts, const int32_t* b_index, int G,
+                     long long M_total, long long M_cap, int N, int K, int swiglu, cudaStream_t s);
+int quant_rows_e4m3(const void* src, long long lds, void* dst, long long ldd, long long rows,
+                    const int32_t* rows_dev, int cols, cudaStream_t s);
 int launch_rowsrc_slot(const DevView& v, cudaStream_t s);
 int launch_rowsrc_token(const DevView& v, cudaStream_t s);
 

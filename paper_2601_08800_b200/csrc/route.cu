@@ -301,14 +301,31 @@ __global__ void __launch_bounds__(512) k_layout(DevView v) {
     if (pub) at<int>(v, v.rank, v.off.exp_cnt)[e] = tot;
     run += tot;
   }
-  s_part[threadIdx.x] = run;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int t = 0; t < (int)blockDim.x; ++t) { const int x = s_part[t]; s_part[t] = acc; acc += x; }
+  {  // block-wide exclusive scan of the per-thread totals (warp shuffles)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_part[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = blockDim.x >> 5;
+      const int x = lane < nw ? s_part[lane] : 0;
+      int wincl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+        if (lane >= o) wincl += y;
+      }
+      if (lane < nw) s_part[lane] = wincl - x;
+    }
+    __syncthreads();
+    run = s_part[wid] + incl - run;
+    __syncthreads();
   }
-  __syncthreads();
-  run = s_part[threadIdx.x];
   for (int e = e_lo; e < e_hi; ++e) {  // global exclusive prefix of totals
     const int tot = s_exp_off[e];
     s_exp_off[e] = run;

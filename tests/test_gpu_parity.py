@@ -372,3 +372,61 @@ def test_wire_token_swiglu_emulated(shape):
     y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
     assert orc.verify_metric(y.float().cpu().numpy(), y_o) <= 2e-2
     plan.close()
+
+
+# ----------------------------------------------------------------- fp8 (config C)
+def test_quant_rows_e4m3_bit_exact():
+    from paper_2601_08800_b200 import _native
+    R, Cc = 300, 1792
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = (torch.randn(R, Cc, device="cuda", generator=gen) * 3).to(torch.bfloat16)
+    x[5] = 0
+    x[7, 11] = 1e4
+    ld = Cc + 16
+    q = torch.zeros(R, ld, dtype=torch.uint8, device="cuda")
+    _native.call("mx_quant_rows_e4m3", x.data_ptr(), Cc, q.data_ptr(), ld, R, Cc,
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    vals = q[:, :Cc].contiguous().view(torch.float8_e4m3fn).float().cpu().numpy()
+    scales = q[:, Cc:Cc + 4].contiguous().view(torch.float32)[:, 0].cpu().numpy()
+    q_ref, s_ref = orc.quant_rows_e4m3(x.float().cpu().numpy())
+    assert np.array_equal(scales, s_ref)
+    assert np.array_equal(vals, q_ref)
+
+
+@pytest.mark.parametrize("swiglu", [False, True])
+def test_grouped_gemm_fp8_vs_dequantized_torch(swiglu):
+    from paper_2601_08800_b200 import _native
+    G, N, K = 3, 512, 1024
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    cnts = torch.tensor([200, 0, 77], dtype=torch.int32)
+    offs = torch.tensor([0, 200, 200], dtype=torch.int32)
+    M = 277
+    a32 = torch.randn(M, K, device="cuda", generator=gen)
+    lda = K + 16
+    A = torch.zeros(M, lda, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    a16 = a32.to(torch.bfloat16)
+    _native.call("mx_quant_rows_e4m3", a16.data_ptr(), K, A.data_ptr(), lda, M, K, s)
+    w = torch.randn(G, N, K, device="cuda", generator=gen) / K ** 0.5
+    ws = (w.abs().amax(-1) / 448).clamp_min(1e-12)
+    Bq = (w / ws[..., None]).to(torch.float8_e4m3fn)
+    D = torch.zeros(M, N // 2 if swiglu else N, dtype=torch.bfloat16, device="cuda")
+    od, cd = offs.cuda(), cnts.cuda()
+    _native.call("mx_grouped_gemm_fp8", A.data_ptr(), lda, Bq.view(torch.uint8).data_ptr(),
+                 ws.contiguous().data_ptr(), D.data_ptr(), od.data_ptr(), cd.data_ptr(), G, M, N,
+                 K, int(swiglu), s)
+    torch.cuda.synchronize()
+    aq = A[:, :K].contiguous().view(torch.float8_e4m3fn).float()
+    asc = A[:, K:K + 4].contiguous().view(torch.float32)[:, 0]
+    for g in range(G):
+        o, c = int(offs[g]), int(cnts[g])
+        if c == 0:
+            continue
+        ref = (aq[o:o + c] * asc[o:o + c, None]) @ (Bq[g].float() * ws[g][:, None]).T
+        if swiglu:
+            # w13 interleave: per 256-row block, 128 gate rows then 128 up rows
+            blocks = ref.view(c, N // 256, 2, 128)
+            ref = (torch.nn.functional.silu(blocks[:, :, 0]) * blocks[:, :, 1]).reshape(c, N // 2)
+        got = D[o:o + c].float()
+        assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (g, (got - ref).abs().max())
