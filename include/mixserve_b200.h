@@ -48,7 +48,11 @@ extern "C" {
 #define MX_ERR_TIMEOUT -5     /* peer-flag watchdog expired                */
 
 typedef enum { MX_F64 = 0, MX_F32 = 1, MX_BF16 = 2 } mx_dtype;
-typedef enum { MX_EXPERT_AFFINE = 0, MX_EXPERT_SWIGLU = 1 } mx_expert_kind;
+/* SWIGLU_FP8: e4m3 experts with per-output-channel weight scales; tokens are
+ * quantised per row (e4m3 + fp32 scale) before dispatch, so the wire carries
+ * h+16 bytes per row; activations are re-quantised between the GEMMs.  The
+ * layer's input and output stay bf16 (act_dtype MX_BF16).                */
+typedef enum { MX_EXPERT_AFFINE = 0, MX_EXPERT_SWIGLU = 1, MX_EXPERT_SWIGLU_FP8 = 2 } mx_expert_kind;
 /* Wire format between groups.  SLOT: one row per routed slot both ways, the
  * reference's A2A layout (sim:366-369, sim:458-475).  TOKEN: one row per
  * (token, host group) pair -- dispatch dedup and combine pre-reduced per
@@ -90,6 +94,7 @@ typedef struct {
   int expert_kind;    /* mx_expert_kind                                      */
   int renormalize;    /* top-k weights renormalised over the k (logits mode) */
   int wire;           /* mx_wire                                             */
+  int shared_inter;   /* shared expert intermediate size (0: none), SWIGLU_FP8 */
   long long capacity; /* receive rows per host; <=0: worst case T*n*min(k,E/n+1) */
 } mx_plan_desc;
 
@@ -105,6 +110,15 @@ typedef struct {
    * w2:  [E/n, h, I/tp].                                                 */
   const void* w13;
   const void* w2;
+  /* MX_EXPERT_SWIGLU_FP8: e4m3 w13/w2 as above plus fp32 per-output-channel
+   * scales [E/n, 2*I/tp] and [E/n, h]; the shared expert's TP shard
+   * (w13_shared [2*Is/tp, h] interleaved like w13, w2_shared [h, Is/tp]).  */
+  const float* w13_scale;
+  const float* w2_scale;
+  const void* w13_shared;
+  const void* w2_shared;
+  const float* w13_shared_scale;
+  const float* w2_shared_scale;
 } mx_expert_params;
 
 /* ----- library ---------------------------------------------------------- */

@@ -19,7 +19,7 @@ from .costmodel import (CostEstimate, indicators, lambda_ep_baseline,  # noqa: F
                         lambda_mix)
 from .strategy import (ParallelStrategy, check_memory, enumerate_strategies,  # noqa: F401
                        format_strategy, parse_strategy)
-from .simcluster import (ExpertSpec, RouterSpec, SimCluster, SwiGLUExperts,  # noqa: F401
+from .simcluster import (ExpertSpec, FP8SwiGLUExperts, RouterSpec, SimCluster, SwiGLUExperts,  # noqa: F401
                          TraceEvent, build_cluster, build_routing_table,
                          fused_ag_dispatch, fused_rs_combine, moe_oracle,
                          run_moe_block, verify_against_oracle)
@@ -33,7 +33,7 @@ __all__ = [
     "lambda_ep_baseline", "lambda_mix", "load_config", "parse_strategy",
     "select_strategy",
     "AnalyzerError", "CalibrationError", "CapacityError", "ConfigError",
-    "ExpertSpec", "GrammarError", "MoeplanError", "RouterSpec",
+    "ExpertSpec", "FP8SwiGLUExperts", "GrammarError", "MoeplanError", "RouterSpec",
     "SaturationError", "SchedulingError", "SimCluster", "StrategyError",
     "SwiGLUExperts", "TraceEvent", "VerificationError", "build_cluster",
     "build_routing_table", "fused_ag_dispatch", "fused_rs_combine",

@@ -23,7 +23,7 @@ MX_ERR_UNSUPPORTED = -4
 MX_ERR_TIMEOUT = -5
 
 MX_F64, MX_F32, MX_BF16 = 0, 1, 2
-MX_EXPERT_AFFINE, MX_EXPERT_SWIGLU = 0, 1
+MX_EXPERT_AFFINE, MX_EXPERT_SWIGLU, MX_EXPERT_SWIGLU_FP8 = 0, 1, 2
 MX_WIRE_SLOT, MX_WIRE_TOKEN = 0, 1
 (MX_BUF_RECV, MX_BUF_PARTIAL, MX_BUF_Y, MX_BUF_IDS, MX_BUF_WEIGHTS,
  MX_BUF_SLOT_POS, MX_BUF_SLOT_TM, MX_BUF_CNT_ALL, MX_BUF_EXP_OFF,
@@ -40,12 +40,15 @@ class PlanDesc(C.Structure):
                 ("top_k", C.c_int), ("inter", C.c_int),
                 ("act_dtype", C.c_int), ("expert_kind", C.c_int),
                 ("renormalize", C.c_int), ("wire", C.c_int),
-                ("capacity", C.c_longlong)]
+                ("shared_inter", C.c_int), ("capacity", C.c_longlong)]
 
 
 class ExpertParams(C.Structure):
     _fields_ = [("scales", C.c_void_p), ("biases", C.c_void_p),
-                ("w13", C.c_void_p), ("w2", C.c_void_p)]
+                ("w13", C.c_void_p), ("w2", C.c_void_p),
+                ("w13_scale", C.c_void_p), ("w2_scale", C.c_void_p),
+                ("w13_shared", C.c_void_p), ("w2_shared", C.c_void_p),
+                ("w13_shared_scale", C.c_void_p), ("w2_shared_scale", C.c_void_p)]
 
 
 VP, I, LL, SZ = C.c_void_p, C.c_int, C.c_longlong, C.c_size_t

@@ -89,7 +89,20 @@ static int validate(const mx_plan_desc& d) {
   if (d.top_k > MX_KMAX) { set_error("top_k %d exceeds %d", d.top_k, MX_KMAX); return MX_ERR_UNSUPPORTED; }
   if (d.act_dtype < MX_F64 || d.act_dtype > MX_BF16) { set_error("bad act_dtype"); return MX_ERR_INVALID; }
   if (d.wire != MX_WIRE_SLOT && d.wire != MX_WIRE_TOKEN) { set_error("bad wire format"); return MX_ERR_INVALID; }
-  if (d.expert_kind == MX_EXPERT_SWIGLU) {
+  if (d.expert_kind == MX_EXPERT_SWIGLU_FP8) {
+    if (d.act_dtype != MX_BF16) { set_error("fp8 experts take bf16 tokens"); return MX_ERR_UNSUPPORTED; }
+    if (d.inter % d.tp != 0 || (d.inter / d.tp) % 128 != 0) { set_error("inter/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED; }
+    if (d.hidden % 256 != 0) { set_error("fp8 experts need hidden %% 256 == 0"); return MX_ERR_UNSUPPORTED; }
+    if (d.shared_inter < 0 || d.shared_inter % d.tp != 0 || (d.shared_inter / d.tp) % 128 != 0) {
+      set_error("shared_inter/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED;
+    }
+    if ((d.hidden / d.tp) % 16 != 0) { set_error("fp8 wire needs (h/tp) %% 16 == 0"); return MX_ERR_UNSUPPORTED; }
+    if (d.shared_inter > 0 && d.top_k > 8) { set_error("shared expert needs top_k <= 8"); return MX_ERR_UNSUPPORTED; }
+  } else if (d.shared_inter != 0) {
+    set_error("shared experts are supported with SWIGLU_FP8 experts"); return MX_ERR_UNSUPPORTED;
+  }
+  if (d.expert_kind == MX_EXPERT_SWIGLU_FP8) {
+  } else if (d.expert_kind == MX_EXPERT_SWIGLU) {
     if (d.act_dtype != MX_BF16) { set_error("SwiGLU experts run in bf16"); return MX_ERR_UNSUPPORTED; }
     if (d.inter % d.tp != 0 || (d.inter / d.tp) % 128 != 0) { set_error("inter/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED; }
     if (d.hidden % 128 != 0) { set_error("hidden must be a multiple of 128 for the grouped GEMM"); return MX_ERR_UNSUPPORTED; }
@@ -112,12 +125,15 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   const size_t C = (T + MX_CHUNK - 1) / MX_CHUNK;
   const size_t elt = elt_bytes(d.act_dtype);
   const size_t wsz = d.act_dtype == MX_F64 ? 8 : 4;
-  const size_t It = d.expert_kind == MX_EXPERT_SWIGLU ? d.inter / d.tp : 0;
+  const bool fp8 = d.expert_kind == MX_EXPERT_SWIGLU_FP8;
+  const size_t It = d.expert_kind != MX_EXPERT_AFFINE ? d.inter / d.tp : 0;
+  const size_t Ist = fp8 ? d.shared_inter / d.tp : 0;
+  const size_t wrow = fp8 ? h + 16 : h * elt;  // bytes per row on the wire
   o.flags = take(8 * MX_MAXW);
   o.cnt_all = take(4 * n * E);
   o.counters = take(4 * 16);
   o.err = take(4 * 16);
-  o.recv = take((size_t)cap * h * elt);
+  o.recv = take((size_t)cap * wrow);
   o.partial = take((size_t)cap * h * elt);
   o.y = take(T * h * elt);
   o.act = take((size_t)cap * It * 2);
@@ -144,12 +160,18 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   const bool tok = d.wire == MX_WIRE_TOKEN;
   const size_t U = tok ? T * n : 0;
   const size_t KH = kh_of(d);
-  o.xbuf = take(U * h * elt);
+  o.xbuf = take(U * wrow);
   o.recv_src = take(4 * (size_t)cap);
   o.pair_p = take(2 * wsz * U * KH);  // packed {row, weight} entries
   o.pair_w = take(0);
   o.pair_n = take(4 * U);
   o.z = take(U * h * elt);
+  o.xq = take(fp8 ? T * wrow : 0);
+  o.actq = take(fp8 ? (size_t)cap * (It + 16) : 0);
+  o.act_s = take(T * Ist * 2);
+  o.actq_s = take(Ist ? T * (Ist + 16) : 0);
+  o.part_s = take(Ist ? T * h * 2 : 0);
+  o.sh_meta = take(16);
   o.total = p;
   return o;
 }
@@ -314,17 +336,27 @@ int mx_plan_create(mx_comm* c, const mx_plan_desc* d, mx_plan** out) {
   DevView& v = p->base;
   v.n = d->n_group; v.m = d->tp; v.W = c->W;
   v.T = d->tokens; v.h = d->hidden; v.E = d->num_experts; v.k = d->top_k;
-  v.I_t = d->expert_kind == MX_EXPERT_SWIGLU ? d->inter / d->tp : 0;
+
   v.C = (d->tokens + MX_CHUNK - 1) / MX_CHUNK;
   v.elt = elt_bytes(d->act_dtype);
   v.renorm = d->renormalize;
   v.wire = d->wire;
   v.KH = kh_of(*d);
+  v.fp8 = d->expert_kind == MX_EXPERT_SWIGLU_FP8;
+  v.welt = v.fp8 ? 1 : v.elt;
+  v.wrow = v.fp8 ? d->hidden + 16 : d->hidden * v.elt;
+  v.Is_t = v.fp8 ? d->shared_inter / d->tp : 0;
+  v.I_t = d->expert_kind != MX_EXPERT_AFFINE ? d->inter / d->tp : 0;
   v.cap = p->cap;
   v.off = p->off;
   for (int r = 0; r < c->W; ++r) v.heap[r] = c->heap[r];
   c->off = p->off;
   c->has_plan = true;
+  {
+    const int meta[4] = {0, d->tokens, 0, 0};
+    for (int r = 0; r < c->W; ++r)
+      if (c->owned[r]) MX_CUDA(cudaMemcpy(c->heap[r] + p->off.sh_meta, meta, sizeof(meta), cudaMemcpyHostToDevice));
+  }
   *out = p;
   return MX_OK;
 }
@@ -477,6 +509,12 @@ int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream) {
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
     const char* xg = group_ptr(p, x, v.group, row);
+    if (v.fp8) {  // e4m3 rows + scale: the wire and GEMM1 operate on these
+      char* xq = p->comm->heap[r] + p->off.xq;
+      rc = quant_rows_e4m3(xg, v.h, xq, v.wrow, v.T, nullptr, v.h, s);
+      if (rc) return rc;
+      xg = xq;
+    }
     if (p->d.wire == MX_WIRE_TOKEN) {
       rc = launch_dispatch_token(v, xg, s);
       p->a_src[r] = gathers(p) ? static_cast<const void*>(p->comm->heap[r] + p->off.xbuf) : nullptr;
@@ -514,6 +552,22 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
     }
     if (p->d.expert_kind == MX_EXPERT_AFFINE) {
       if (stage != 2) rc = launch_expert_affine(v, ep->scales, ep->biases, s);
+    } else if (v.fp8) {
+      mx_expert_params e = *ep;
+      if (p->comm->emulate) {  // per-rank shards stacked rank-major
+        const size_t El = (v.E + v.n - 1) / v.n;
+        e.w13 = static_cast<const char*>(ep->w13) + r * El * 2 * v.I_t * v.h;
+        e.w2 = static_cast<const char*>(ep->w2) + r * El * v.h * v.I_t;
+        e.w13_scale = ep->w13_scale + r * El * 2 * v.I_t;
+        e.w2_scale = ep->w2_scale + r * El * v.h;
+        if (v.Is_t) {
+          e.w13_shared = static_cast<const char*>(ep->w13_shared) + (size_t)r * 2 * v.Is_t * v.h;
+          e.w2_shared = static_cast<const char*>(ep->w2_shared) + (size_t)r * v.h * v.Is_t;
+          e.w13_shared_scale = ep->w13_shared_scale + (size_t)r * 2 * v.Is_t;
+          e.w2_shared_scale = ep->w2_shared_scale + (size_t)r * v.h;
+        }
+      }
+      rc = launch_expert_fp8(v, e, stage, s);
     } else {
       // emulated: per-rank weight shards stacked rank-major
       const int Elmax = (v.E + v.n - 1) / v.n;

@@ -109,6 +109,13 @@ __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
               for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(ws[s], red[s][q]));
             }
         }
+        if (v.Is_t)  // shared expert: TP partials of the group's own tokens
+          for (int tt = 0; tt < m; ++tt) {
+            const uint4 raw = ld_v4(at<T>(v, j * m + tt, v.off.part_s) + (size_t)tl * h + c);
+            const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
+          }
         // final intra-group all-gather: push the shard to every TP rank
         for (int tt = 0; tt < m; ++tt) {
           T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)tl * h + c;

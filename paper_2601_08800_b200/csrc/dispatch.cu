@@ -53,10 +53,12 @@ __global__ void __launch_bounds__(256) k_dispatch(DevView v, const char* __restr
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const int* ids = at<int>(v, v.rank, v.off.ids);
   const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
-  const size_t row_bytes = (size_t)v.h * v.elt;
+  const size_t row_bytes = (size_t)v.wrow;  // wire row (e4m3 rows carry a scale tail)
+  const size_t body = (size_t)v.h * v.welt;
   int c0, c1;
   col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
-  const size_t sh_off = (size_t)c0 * v.elt, sh_bytes = (size_t)(c1 - c0) * v.elt;
+  const size_t sh_off = (size_t)c0 * v.welt, sh_bytes = (size_t)(c1 - c0) * v.welt;
+  const bool tail = v.tp_rank == 0 && row_bytes > body;  // TP rank 0 ships the scale
   const long long total = (long long)v.T * v.k;
   for (long long s = gw; s < total; s += nwarps) {
     const int t = (int)(s / v.k);
@@ -70,8 +72,9 @@ __global__ void __launch_bounds__(256) k_dispatch(DevView v, const char* __restr
       warp_copy(at<char>(v, v.rank, v.off.recv) + pos * row_bytes, row, row_bytes, lane);
     } else {
       for (int tt = 0; tt < v.m; ++tt) {
-        char* dst = at<char>(v, d * v.m + tt, v.off.recv) + pos * row_bytes + sh_off;
-        warp_copy(dst, row + sh_off, sh_bytes, lane);
+        char* dst = at<char>(v, d * v.m + tt, v.off.recv) + pos * row_bytes;
+        warp_copy(dst + sh_off, row + sh_off, sh_bytes, lane);
+        if (tail) warp_copy(dst + body, row + body, row_bytes - body, lane);
       }
     }
   }

@@ -632,6 +632,55 @@ int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b
                 : launch<256, false, false, true>(ma, mb, md, a, max_tiles, s);
 }
 
+// fp8 experts of one rank (BASELINE config C): e4m3 GEMM1 + SwiGLU -> bf16
+// act -> per-row e4m3 re-quantisation -> e4m3 GEMM2 -> bf16 TP partial; the
+// shared expert runs the same two GEMMs on the group's own tokens (one
+// "group" of T rows) into part_s, which the combine adds.
+int launch_expert_fp8(const DevView& v, const mx_expert_params& ep, int stage, cudaStream_t s) {
+  const int e0 = first_expert(v.group, v.n, v.E), e1 = first_expert(v.group + 1, v.n, v.E);
+  const int El = e1 - e0;
+  const int32_t* offs = at<int32_t>(v, v.rank, v.off.exp_off) + e0;
+  const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
+  const int32_t* sh = at<int32_t>(v, v.rank, v.off.sh_meta);
+  const int* host_rows = at<int>(v, v.rank, v.off.host_rows) + v.group;
+  int rc = MX_OK;
+  if (stage != 2) {
+    if (El > 0) {
+      rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.recv), v.wrow, ep.w13, ep.w13_scale,
+                            at<char>(v, v.rank, v.off.act), offs, cnts, nullptr, El, v.cap, v.cap,
+                            2 * v.I_t, v.h, 1, s);
+      if (rc) return rc;
+      rc = quant_rows_e4m3(at<char>(v, v.rank, v.off.act), v.I_t, at<char>(v, v.rank, v.off.actq),
+                           v.I_t + 16, v.cap, host_rows, v.I_t, s);
+      if (rc) return rc;
+    }
+    if (v.Is_t && v.T > 0) {
+      rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.xq), v.wrow, ep.w13_shared, ep.w13_shared_scale,
+                            at<char>(v, v.rank, v.off.act_s), sh, sh + 1, nullptr, 1, v.T, v.T,
+                            2 * v.Is_t, v.h, 1, s);
+      if (rc) return rc;
+      rc = quant_rows_e4m3(at<char>(v, v.rank, v.off.act_s), v.Is_t,
+                           at<char>(v, v.rank, v.off.actq_s), v.Is_t + 16, v.T, nullptr, v.Is_t, s);
+      if (rc) return rc;
+    }
+  }
+  if (stage != 1) {
+    if (El > 0) {
+      rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.actq), v.I_t + 16, ep.w2, ep.w2_scale,
+                            at<char>(v, v.rank, v.off.partial), offs, cnts, nullptr, El, v.cap,
+                            v.cap, v.h, v.I_t, 0, s);
+      if (rc) return rc;
+    }
+    if (v.Is_t && v.T > 0) {
+      rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.actq_s), v.Is_t + 16, ep.w2_shared,
+                            ep.w2_shared_scale, at<char>(v, v.rank, v.off.part_s), sh, sh + 1,
+                            nullptr, 1, v.T, v.T, v.h, v.Is_t, 0, s);
+      if (rc) return rc;
+    }
+  }
+  return rc;
+}
+
 // Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.
 int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
                          cudaStream_t s) {

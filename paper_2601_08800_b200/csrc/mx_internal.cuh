@@ -67,6 +67,13 @@ struct Offsets {
   size_t pair_w;      // AccT [T*n][KH]  slot weights of a pair (peers write)
   size_t pair_n;      // int32 [T*n]     slots of a pair (peers write)
   size_t z;           // act [T*n][h]  pre-reduced w*partial per pair (peers read)
+  // fp8 experts (SWIGLU_FP8) and the shared expert
+  size_t xq;          // [T][wrow]       this group's tokens, e4m3 + row scale
+  size_t actq;        // [cap][I_t+16]   e4m3 activation + row scale (GEMM2 A)
+  size_t act_s;       // bf16 [T][Is_t]  shared expert activation
+  size_t actq_s;      // [T][Is_t+16]
+  size_t part_s;      // bf16 [T][h]     shared expert TP partial (peers read)
+  size_t sh_meta;     // int32 [4]       {0, T} offs/cnt of the shared "group"
   size_t counters;    // int32 [16]  [0]=route CTA counter [2..3]=u64 barrier epoch
   size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
   size_t total;
@@ -79,6 +86,10 @@ struct DevView {
   int renorm;
   int wire;           // mx_wire
   int KH;             // max slots of one token on one host
+  int welt;           // bytes per element on the wire (1: e4m3)
+  int wrow;           // bytes per row on the wire (h*welt [+16 scale tail])
+  int fp8;            // SWIGLU_FP8 plan
+  int Is_t;           // shared expert intermediate per TP rank (0: none)
   const void* a_src;  // GEMM1 gathers A rows from here (x or XBUF), nullptr: RECV
   long long a_src_rows;
   long long cap;
@@ -167,6 +178,7 @@ int launch_expert_affine(const DevView& v, const void* scales, const void* biase
                          cudaStream_t s);
 int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
                          cudaStream_t s);
+int launch_expert_fp8(const DevView& v, const mx_expert_params& ep, int stage, cudaStream_t s);
 int launch_combine(const DevView& v, cudaStream_t s);
 int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s);
 int launch_expand(const DevView& v, cudaStream_t s);

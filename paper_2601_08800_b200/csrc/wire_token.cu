@@ -52,10 +52,12 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
   const WT* wts = at<WT>(v, v.rank, v.off.w);
   const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
   const int* upos = at<int>(v, v.rank, v.off.upos);
-  const size_t row_bytes = (size_t)v.h * v.elt;
+  const size_t row_bytes = (size_t)v.wrow;
+  const size_t body = (size_t)v.h * v.welt;
   int c0, c1;
   col_shard(v.h, m, v.tp_rank, &c0, &c1);
-  const size_t sh_off = (size_t)c0 * v.elt, sh_bytes = (size_t)(c1 - c0) * v.elt;
+  const size_t sh_off = (size_t)c0 * v.welt, sh_bytes = (size_t)(c1 - c0) * v.welt;
+  const bool tail = v.tp_rank == 0 && row_bytes > body;
   for (long long t = gw; t < v.T; t += nwarps) {
     const char* row = x + (size_t)t * row_bytes;
     for (int d = 0; d < n; ++d) {
@@ -64,9 +66,11 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
       if (d == v.group) {
         copy_row(at<char>(v, v.rank, v.off.xbuf) + (size_t)u * row_bytes, row, row_bytes, lane);
       } else {
-        for (int tt = 0; tt < m; ++tt)
-          copy_row(at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes + sh_off,
-                   row + sh_off, sh_bytes, lane);
+        for (int tt = 0; tt < m; ++tt) {
+          char* dst = at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes;
+          copy_row(dst + sh_off, row + sh_off, sh_bytes, lane);
+          if (tail) copy_row(dst + body, row + body, row_bytes - body, lane);
+        }
       }
     }
     // metadata: lane i carries slot i
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
   const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
-  const size_t row_bytes = (size_t)v.h * v.elt;
+  const size_t row_bytes = (size_t)v.wrow;
   const char* xbuf = at<char>(v, v.rank, v.off.xbuf);
   char* recv = at<char>(v, v.rank, v.off.recv);
   for (long long u = gw; u < pairs; u += nwarps) {
@@ -222,6 +226,13 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
             for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
           }
       }
+      if (v.Is_t)  // shared expert: TP partials of the group's own tokens
+        for (int tt = 0; tt < m; ++tt) {
+          const uint4 raw = ld_v4(at<T>(v, j * m + tt, v.off.part_s) + (size_t)t * h + c);
+          const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
+        }
       T out[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);

@@ -53,7 +53,7 @@ class LayerPlan:
     def __init__(self, n, m, tokens, hidden, num_experts, top_k, *,
                  dtype=torch.float64, expert_kind="affine", inter=0,
                  renormalize=True, capacity=None, emulate=True, rank=None,
-                 process_group=None, device=None, wire="slot"):
+                 process_group=None, device=None, wire="slot", shared_inter=0):
         lib = N.load()
         if not torch.cuda.is_available():
             raise N.NativeLibraryError("no CUDA device: the MoE layer runs "
@@ -72,9 +72,11 @@ class LayerPlan:
             torch.device("cuda", torch.cuda.current_device())
         self.desc = N.PlanDesc(
             n, m, tokens, hidden, num_experts, top_k, inter, DTYPES[dtype],
-            N.MX_EXPERT_SWIGLU if expert_kind == "swiglu" else N.MX_EXPERT_AFFINE,
+            {"swiglu": N.MX_EXPERT_SWIGLU, "swiglu_fp8": N.MX_EXPERT_SWIGLU_FP8}.get(
+                expert_kind, N.MX_EXPERT_AFFINE),
             1 if renormalize else 0,
-            N.MX_WIRE_TOKEN if wire == "token" else N.MX_WIRE_SLOT, int(capacity or 0))
+            N.MX_WIRE_TOKEN if wire == "token" else N.MX_WIRE_SLOT, int(shared_inter),
+            int(capacity or 0))
         self.wire = wire
         heap = C.c_size_t()
         N.check(lib.mx_plan_heap_bytes(C.byref(self.desc), C.byref(heap)),

@@ -41,7 +41,7 @@ from .trace import (FLOAT_BYTES, TRACE_CSV_HEADER, Trace, TraceBuilder,
 __all__ = [
     "FLOAT_BYTES", "SimRank", "SimCluster", "build_cluster", "TraceEvent",
     "Trace", "TRACE_CSV_HEADER", "trace_to_csv", "trace_from_csv",
-    "save_trace", "RouterSpec", "ExpertSpec", "SwiGLUExperts",
+    "save_trace", "RouterSpec", "ExpertSpec", "SwiGLUExperts", "FP8SwiGLUExperts",
     "expert_home_node", "Slot", "RoutingTable", "build_routing_table",
     "ref_reduce_scatter", "ref_all_gather", "ref_all_reduce",
     "ref_all_to_all_pairwise", "moe_oracle", "fused_ag_dispatch",
@@ -250,6 +250,115 @@ class SwiGLUExperts:
         return w13, w2
 
 
+def _quant_rows_torch(w):
+    """Per-row e4m3 weights: scale = amax/448 (fp32), values (w/scale) rounded
+    to e4m3 (RNE; |w/scale| <= 448 by construction)."""
+    w = w.float()
+    s = (w.abs().amax(-1) / 448.0).clamp_min(1e-30)
+    return (w / s[..., None]).to(torch.float8_e4m3fn), s.contiguous()
+
+
+class FP8SwiGLUExperts:
+    """fp8 (e4m3) SwiGLU experts + optional shared expert (BASELINE config C,
+    DeepSeek-R1 shape: 256 routed + 1 shared, fp8 experts).
+
+    Each rank's TP shard is quantised per output channel (row) after
+    sharding; tokens are quantised per row by the layer before dispatch and
+    the activation is re-quantised per row of each TP shard between the two
+    GEMMs.  ``shared`` is a one-expert :class:`SwiGLUExperts` applied to
+    every token with weight 1, TP-sharded inside each group."""
+
+    def __init__(self, experts: SwiGLUExperts, shared: SwiGLUExperts | None = None):
+        self.src, self.shared = experts, shared
+        self.E, self.I, self.h = experts.E, experts.I, experts.h
+        self.Is = shared.I if shared is not None else 0
+        self._cache = {}
+
+    @classmethod
+    def random(cls, num_experts, hidden, inter, shared_inter=0, seed=0, device="cuda"):
+        ex = SwiGLUExperts.random(num_experts, hidden, inter, seed=seed, device=device)
+        sh = (SwiGLUExperts.random(1, hidden, shared_inter, seed=seed + 7919, device=device)
+              if shared_inter else None)
+        return cls(ex, sh)
+
+    @property
+    def num_experts(self) -> int:
+        return self.E
+
+    def rank_shard(self, n, m, rank):
+        """dict of this rank's e4m3 shards (uint8 views) and fp32 scales."""
+        key = (n, m, rank)
+        if key in self._cache:
+            return self._cache[key]
+        w13, w2 = self.src.rank_shard(n, m, rank)
+        out = {}
+        out["w13"], out["w13_scale"] = _quant_rows_torch(w13)
+        out["w2"], out["w2_scale"] = _quant_rows_torch(w2)
+        if self.shared is not None:
+            s13, s2 = self.shared.rank_shard(1, m, rank % m)
+            out["w13_shared"], out["w13_shared_scale"] = _quant_rows_torch(s13[0])
+            out["w2_shared"], out["w2_shared_scale"] = _quant_rows_torch(s2[0])
+        self._cache[key] = out
+        return out
+
+    def stacked_shards(self, n, m):
+        key = ("stack", n, m)
+        if key in self._cache:
+            return self._cache[key]
+        per = [self.rank_shard(n, m, r) for r in range(n * m)]
+        el = max(p["w13"].shape[0] for p in per)
+        out = {}
+        for name, t in per[0].items():
+            full = torch.zeros((n * m, el) + tuple(t.shape[1:]) if name in ("w13", "w2", "w13_scale", "w2_scale")
+                               else (n * m,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            for r, p in enumerate(per):
+                if name in ("w13", "w2", "w13_scale", "w2_scale"):
+                    full[r, :p[name].shape[0]] = p[name]
+                else:
+                    full[r] = p[name]
+            out[name] = full
+        self._cache[key] = out
+        return out
+
+    def params(self, shards):
+        ptr = lambda name: shards[name].data_ptr() if name in shards else None
+        return N.ExpertParams(None, None, ptr("w13"), ptr("w2"), ptr("w13_scale"),
+                              ptr("w2_scale"), ptr("w13_shared"), ptr("w2_shared"),
+                              ptr("w13_shared_scale"), ptr("w2_shared_scale"))
+
+    def oracle_arrays(self, n, m):
+        """Dequantised per-(rank shard) weights for the CPU replica:
+        gate/up [E, m, It, h], down [E, m, h, It] (+ shared [m, ...])."""
+        It = self.I // m
+        gate = np.zeros((self.E, m, It, self.h), np.float32)
+        up = np.zeros_like(gate)
+        down = np.zeros((self.E, m, self.h, It), np.float32)
+        sh = None
+        for r in range(n * m):
+            d, t = divmod(r, m)
+            e0 = -(-d * self.E // n)
+            p = self.rank_shard(n, m, r)
+            w13 = (p["w13"].float() * p["w13_scale"][..., None]).cpu().numpy()
+            w2 = (p["w2"].float() * p["w2_scale"][..., None]).cpu().numpy()
+            for i in range(w13.shape[0]):
+                blocks = w13[i].reshape(-1, 2, 128, self.h)
+                gate[e0 + i, t] = blocks[:, 0].reshape(It, self.h)
+                up[e0 + i, t] = blocks[:, 1].reshape(It, self.h)
+                down[e0 + i, t] = w2[i]
+            if self.shared is not None and d == 0:
+                if sh is None:
+                    Ist = self.Is // m
+                    sh = [np.zeros((m, Ist, self.h), np.float32),
+                          np.zeros((m, Ist, self.h), np.float32),
+                          np.zeros((m, self.h, Ist), np.float32)]
+                s13 = (p["w13_shared"].float() * p["w13_shared_scale"][..., None]).cpu().numpy()
+                blocks = s13.reshape(-1, 2, 128, self.h)
+                sh[0][t] = blocks[:, 0].reshape(-1, self.h)
+                sh[1][t] = blocks[:, 1].reshape(-1, self.h)
+                sh[2][t] = (p["w2_shared"].float() * p["w2_shared_scale"][..., None]).cpu().numpy()
+        return gate, up, down, sh
+
+
 def expert_home_node(expert, n_node, num_experts):
     """Contiguous block placement (sim:210-212)."""
     return expert * n_node // num_experts
@@ -298,13 +407,14 @@ class RoutingTable:
 _PLANS: "OrderedDict[tuple, LayerPlan]" = OrderedDict()
 
 
-def _plan(n, m, T, h, E, k, dtype, kind="affine", inter=0, capacity=None):
-    key = (n, m, T, h, E, k, dtype, kind, inter, capacity,
+def _plan(n, m, T, h, E, k, dtype, kind="affine", inter=0, capacity=None, shared_inter=0):
+    key = (n, m, T, h, E, k, dtype, kind, inter, capacity, shared_inter,
            torch.cuda.current_device())
     p = _PLANS.get(key)
     if p is None:
         p = LayerPlan(n, m, T, h, E, k, dtype=dtype, expert_kind=kind,
-                      inter=inter, capacity=capacity, emulate=True)
+                      inter=inter, capacity=capacity, emulate=True,
+                      shared_inter=shared_inter)
         _PLANS[key] = p
         while len(_PLANS) > 4:
             _PLANS.popitem(last=False)[1].close()
@@ -337,6 +447,9 @@ def _router_tensors(router, wdtype):
 
 def _expert_params(plan, experts, dtype):
     """ExpertParams struct + the tensors it points to (kept alive)."""
+    if isinstance(experts, FP8SwiGLUExperts):
+        sh = experts.stacked_shards(plan.n, plan.m)
+        return experts.params(sh), sh
     if isinstance(experts, SwiGLUExperts):
         w13, w2 = experts.stacked_shards(plan.n, plan.m)
         return N.ExpertParams(None, None, w13.data_ptr(), w2.data_ptr()), (w13, w2)
@@ -349,6 +462,8 @@ def _expert_params(plan, experts, dtype):
 
 
 def _kind(experts):
+    if isinstance(experts, FP8SwiGLUExperts):
+        return "swiglu_fp8"
     return "swiglu" if isinstance(experts, SwiGLUExperts) else "affine"
 
 
@@ -616,14 +731,15 @@ def run_moe_block(cluster: SimCluster, x_global, router: RouterSpec, experts,
                             f"carries {x_global.shape[0]}")
     numpy_in = not isinstance(x_global, torch.Tensor)
     kind = _kind(experts)
-    if kind == "swiglu":
+    if kind in ("swiglu", "swiglu_fp8"):
         dtype = torch.bfloat16
     else:
         dtype = torch.float64 if numpy_in else x_global.dtype
     xg = _to_dev(x_global, dtype).contiguous()
     ids, _ = router.arrays()
     plan = _plan(n, m, T, h, router.num_experts, ids.shape[1], dtype, kind,
-                 experts.I if kind == "swiglu" else 0, capacity)
+                 experts.I if kind != "affine" else 0, capacity,
+                 experts.Is if kind == "swiglu_fp8" else 0)
     params, keep = _expert_params(plan, experts, dtype)
     _route(plan, router, check_capacity=True)
     cnt = plan.rank_views(0)["cnt_all"].cpu().numpy().astype(np.int64)

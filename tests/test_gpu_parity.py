@@ -430,3 +430,41 @@ def test_grouped_gemm_fp8_vs_dequantized_torch(swiglu):
             ref = (torch.nn.functional.silu(blocks[:, :, 0]) * blocks[:, :, 1]).reshape(c, N // 2)
         got = D[o:o + c].float()
         assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (g, (got - ref).abs().max())
+
+
+def _fp8_case(n, m, T, h, E, k, I, Is, wire="slot", seed=1):
+    from paper_2601_08800_b200 import FP8SwiGLUExperts, RouterSpec, build_cluster, run_moe_block
+    from paper_2601_08800_b200 import _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    ex = FP8SwiGLUExperts.random(E, h, I, shared_inter=Is, seed=seed)
+    gen = torch.Generator(device="cuda").manual_seed(seed + 1)
+    x = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    router = RouterSpec.random(n * T, E, k, seed=seed + 2)
+    if wire == "slot":
+        y, _ = run_moe_block(build_cluster(n, m), x, router, ex)
+    else:
+        plan = LayerPlan(n, m, T, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu_fp8",
+                         inter=I, shared_inter=Is, wire=wire)
+        sh = ex.stacked_shards(n, m)
+        ids, w = router.arrays()
+        y = torch.empty(n * T, h, dtype=torch.bfloat16, device="cuda")
+        plan.forward(x, ex.params(sh), ids=torch.as_tensor(ids).cuda(),
+                     weights=torch.as_tensor(w, dtype=torch.float32).cuda(), y_out=y)
+        plan.close()
+    gate, up, down, shared = ex.oracle_arrays(n, m)
+    ids, w = router.arrays()
+    y_o = orc.moe_layer_fp8(x.float().cpu().numpy(), ids, w, gate, up, down, shared)
+    return orc.verify_metric(y.float().cpu().numpy(), y_o)
+
+
+@pytest.mark.parametrize("n,m,Is,wire", [(1, 1, 0, "slot"), (2, 2, 256, "slot"), (2, 4, 512, "slot"),
+                                         (4, 2, 256, "token"), (2, 4, 512, "token")])
+def test_fp8_layer_vs_oracle(n, m, Is, wire):
+    assert _fp8_case(n, m, 48, 512, 16, 4, 512, Is, wire) <= 2e-2
+
+
+def test_fp8_deepseek_shape_layer():
+    """BASELINE configs[2] shape: h=7168, moe_intermediate=2048, top-8 with a
+    2048-wide shared expert, TP4 x EP2 (emulated 8 ranks on one GPU); expert
+    count reduced to 16 to keep the fp8 weights in the test's budget."""
+    assert _fp8_case(2, 4, 16, 7168, 16, 8, 2048, 2048, "slot", seed=11) <= 2e-2

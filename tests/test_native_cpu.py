@@ -34,15 +34,15 @@ def test_library_loads_and_exports_every_header_symbol():
 def test_plan_heap_bytes_and_validation_map_to_reference_errors():
     lib = N.load()
     d = N.PlanDesc(4, 2, 2048, 2048, 128, 8, 768, N.MX_BF16,
-                   N.MX_EXPERT_SWIGLU, 1, N.MX_WIRE_SLOT, 0)
+                   N.MX_EXPERT_SWIGLU, 1, N.MX_WIRE_SLOT, 0, 0)
     out = C.c_size_t()
     N.check(lib.mx_plan_heap_bytes(C.byref(d), C.byref(out)))
     # worst-case capacity: T*n*min(k, E/n) rows of h bf16, twice (recv+partial)
     assert out.value > 2 * 2048 * 4 * 8 * 2048 * 2
-    bad = N.PlanDesc(0, 2, 8, 8, 8, 2, 0, N.MX_F64, 0, 1, 0, 0)
+    bad = N.PlanDesc(0, 2, 8, 8, 8, 2, 0, N.MX_F64, 0, 1, 0, 0, 0)
     with pytest.raises(StrategyError, match="at least one node"):
         N.check(lib.mx_plan_heap_bytes(C.byref(bad), C.byref(out)))
-    bad = N.PlanDesc(2, 2, 8, 8, 8, 9, 0, N.MX_F64, 0, 1, 0, 0)
+    bad = N.PlanDesc(2, 2, 8, 8, 8, 9, 0, N.MX_F64, 0, 1, 0, 0, 0)
     with pytest.raises(StrategyError, match="top_k"):
         N.check(lib.mx_plan_heap_bytes(C.byref(bad), C.byref(out)))
 
