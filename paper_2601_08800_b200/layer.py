@@ -22,7 +22,7 @@ import torch.distributed as dist
 
 from . import _native as N
 from .plan import LayerPlan, stream_ptr
-from .simcluster import SwiGLUExperts
+from .simcluster import FP8SwiGLUExperts, SwiGLUExperts
 
 
 def layout_for(world: int, tp: int | None = None):
@@ -49,13 +49,20 @@ class MoELayer:
         self.T, self.h, self.E, self.k, self.I = (tokens_per_group, hidden,
                                                   num_experts, top_k, inter)
         self.dtype = dtype
+        if isinstance(experts, FP8SwiGLUExperts):
+            expert_kind = "swiglu_fp8"
+        shared_inter = experts.Is if expert_kind == "swiglu_fp8" else 0
         self.plan = LayerPlan(n, m, tokens_per_group, hidden, num_experts,
                               top_k, dtype=dtype, expert_kind=expert_kind,
                               inter=inter, renormalize=renormalize,
                               capacity=capacity, emulate=False, rank=rank,
-                              process_group=process_group, wire=wire)
+                              process_group=process_group, wire=wire,
+                              shared_inter=shared_inter)
         self.wire = wire
-        if expert_kind == "swiglu":
+        if expert_kind == "swiglu_fp8":
+            self.shards = experts.rank_shard(n, m, rank)
+            self.params = experts.params(self.shards)
+        elif expert_kind == "swiglu":
             if w13 is None:
                 w13, w2 = experts.rank_shard(n, m, rank)
             self.w13, self.w2 = w13, w2

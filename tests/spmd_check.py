@@ -117,6 +117,33 @@ def main():
                 failures.append(f"swiglu baseline rank {r}: err {e2:.3e}")
     layer.close()
 
+    # ---------------- fp8 experts + shared expert (config C path), both wires
+    from paper_2601_08800_b200 import FP8SwiGLUExperts
+    T, h, E, k, I, Is = 64, 512, 16, 4, 512, 512
+    fex = FP8SwiGLUExperts.random(E, h, I, shared_inter=Is, seed=21)
+    x8 = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    l8 = torch.randn(n * T, E, device="cuda", generator=gen)
+    xs8, ls8 = x8[g * T:(g + 1) * T].contiguous(), l8[g * T:(g + 1) * T].contiguous()
+    outs = {}
+    for wire in ("slot", "token"):
+        layer = MoELayer(n, m, T, h, E, k, I, experts=fex, rank=rank, wire=wire)
+        outs[wire] = gather_rows(layer.forward(xs8, ls8).clone(), world)
+        layer.close()
+    if rank == 0:
+        gate, up, down, shared = fex.oracle_arrays(n, m)
+        ids, w = orc.router_topk(l8.cpu().numpy(), k)
+        y_ref = orc.moe_layer_fp8(x8.float().cpu().numpy(), ids, w, gate, up, down, shared)
+        for wire, ys8 in outs.items():
+            for r in range(world):
+                gg = r // m
+                ref = y_ref[gg * T:(gg + 1) * T]
+                got = ys8[r].double().cpu().numpy()
+                fro = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+                mx = orc.verify_metric(got, ref)
+                if fro > 1e-2 or mx > 5e-2:
+                    failures.append(f"fp8 {wire} rank {r}: fro {fro:.3e} max {mx:.3e}")
+        print(f"fp8 layer checked over slot/token wires", flush=True)
+
     flag = torch.tensor([len(failures)], device="cuda")
     dist.all_reduce(flag)
     if rank == 0:
