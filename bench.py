@@ -124,7 +124,7 @@ def cpu_oracle_step(x, logits, experts_np):
     return orc.moe_layer_swiglu(x, ids, w, experts_np)
 
 
-def cpu_baseline(sample_tokens=512, reps=3, seed=0):
+def cpu_baseline(sample_tokens=512, reps=3, seed=0, target_s=10.0):
     import torch
     from paper_2601_08800_b200 import SwiGLUExperts
     from oracle import mixserve_oracle as orc
@@ -137,6 +137,10 @@ def cpu_baseline(sample_tokens=512, reps=3, seed=0):
     logits = rng.standard_normal((sample_tokens, E)).astype(np.float32)
     cpu_oracle_step(x[:64], logits[:64], onp)   # warm BLAS
     t0 = time.perf_counter()
+    cpu_oracle_step(x, logits, onp)
+    one = time.perf_counter() - t0
+    reps = max(reps, int(np.ceil(target_s / max(one, 1e-3))))  # ~target_s of CPU work
+    t0 = time.perf_counter()
     for _ in range(reps):
         cpu_oracle_step(x, logits, onp)
     dt = (time.perf_counter() - t0) / reps
@@ -144,7 +148,8 @@ def cpu_baseline(sample_tokens=512, reps=3, seed=0):
     return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": threads,
             "kind": "port",
             "sample": f"{sample_tokens} tokens of the {T_GLOBAL}-token Qwen3-shape batch "
-                      f"(oracle gate + SwiGLU experts, f32 numpy/BLAS), best of {reps}",
+                      f"(oracle gate + SwiGLU experts, f32 numpy/BLAS), mean of {reps} "
+                      f"repetitions (~{target_s:.0f} s of CPU work)",
             "seconds_per_sample": dt}
 
 
