@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -498,6 +499,276 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   }
 }
 
+// ------------------------------------------------------------ CTA pair (2SM)
+// tcgen05.mma.cta_group::2, M=256 x N=256 tiles: CTA rank c of the cluster
+// pair loads A rows [c*128, c*128+128) and B rows [c*128, c*128+128) of the
+// tile into its own shared memory; the leader (rank 0) issues every MMA,
+// which reads both CTAs' operands, and each CTA's TMEM holds its 128 rows x
+// 256 columns of the accumulator.  Per SM, a 512-cycle k-block needs 32 KB
+// of operands instead of 48 KB (M=128 single-CTA) -- the single-CTA kernel
+// is bound by that L2->SM feed (GEMM1 ran at the same time at 1.45 and
+// 1.97 GHz, profiles/r01).
+constexpr int P_STAGES = 6;
+constexpr int P_A = 128 * BKB;              // per CTA: 128 A rows
+constexpr int P_B = 128 * BKB;              // per CTA: 128 of the 256 B rows
+constexpr int P_STAGE = P_A + P_B;
+constexpr int P_STAGING = 4 * 2 * 32 * 64;
+constexpr int P_SMEM = P_STAGES * P_STAGE + 1024 + 1024 + P_STAGING;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load that completes on the pair leader's mbarrier (same offset)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int c0, int c1) {
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)0x3)
+      : "memory");
+}
+
+template <bool SWIGLU>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_d, Args args) {
+  constexpr int BN = 256, PM = 256;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + P_STAGES * P_A;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2] (leader's are used)
+  unsigned char* staging = smem + P_STAGES * P_STAGE + 1024;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_tstart[MX_EMAX + 1];
+  __shared__ int s_off[MX_EMAX];
+  __shared__ int s_cnt[MX_EMAX];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int G = args.G, nN = args.N / BN, kblocks = args.K / BK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    s_off[g] = args.offs[g];
+    s_cnt[g] = args.cnts[g];
+  }
+  __syncthreads();
+  if (warp == 3) {
+    int carry = 0;
+    for (int base = 0; base < G; base += 32) {
+      const int g = base + lane;
+      const int tiles = g < G ? ((s_cnt[g] + PM - 1) / PM) * nN : 0;
+      int incl = tiles;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (g < G) s_tstart[g] = carry + incl - tiles;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_tstart[G] = carry;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    tma_prefetch(&map_d);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int st = 0; st < P_STAGES; ++st) {
+      mbar_init(&full[st], 1);   // leader: one arrive.expect_tx for both CTAs' bytes
+      mbar_init(&empty[st], 1);  // one multicast commit per use
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const int total_tiles = s_tstart[G];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs): own half of A rows and of B rows
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total_tiles; t += npairs) {
+        int g, mb, nb;
+        decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+        const int a_row = s_off[g] + mb * PM + (int)crank * 128;
+        const int b_row = g * args.N + nb * BN + (int)crank * 128;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * P_STAGE);
+          tma_load_2d_pair(sA + stage * P_A, &map_a, &full[stage], kb * BK, a_row);
+          tma_load_2d_pair(sB + stage * P_B, &map_b, &full[stage], kb * BK, b_row);
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===== MMA issuer (leader CTA, single thread), M=256 N=256 K=16
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(PM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < total_tiles; t += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * P_A));
+          const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * P_B));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16_pair(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
+          mma_commit_pair(&empty[stage]);  // frees the slot in both CTAs
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc]);  // both CTAs' accumulators ready
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue (both CTAs): thread = row of this CTA's 128-row half
+    const int q = warp & 3;
+    const int row_in_half = q * 32 + lane;
+    unsigned char* my_stage = staging + q * (2 * 32 * 64);
+    const uint32_t tempty_leader0 = map_to_rank(smem_u32(&tempty[0]), 0);
+    int buf = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < total_tiles; t += npairs) {
+      int g, mb, nb;
+      decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+      const int cnt = s_cnt[g];
+      const int r_local = mb * PM + (int)crank * 128 + row_in_half;
+      const bool valid = r_local < cnt;
+      const long long row = (long long)s_off[g] + r_local;
+      const bool full_box = (mb * PM + (int)crank * 128 + q * 32 + 31) < cnt;
+      const int row0 = s_off[g] + mb * PM + (int)crank * 128 + q * 32;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (SWIGLU) {
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.D) + row * args.ldd + nb * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t gr[32], ur[32];
+          tmem_ld32(tbase + c, gr);
+          tmem_ld32(tbase + BN / 2 + c, ur);
+          tmem_wait_ld();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = silu(__uint_as_float(gr[2 * i])) * __uint_as_float(ur[2 * i]);
+            const float a1 = silu(__uint_as_float(gr[2 * i + 1])) * __uint_as_float(ur[2 * i + 1]);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+            packed[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          if (full_box) {
+            stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * (BN / 2) + c, row0);
+            buf ^= 1;
+          } else if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 b2 =
+                __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+            packed[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          if (full_box) {
+            stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * BN + c, row0);
+            buf ^= 1;
+          } else if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.D) +
+                                                  row * args.ldd + nb * BN + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);  // leader's tempty[acc]
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
 // ------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -560,6 +831,30 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   return MX_OK;
 }
 
+template <bool SWIGLU>
+static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+                       const Args& a, long long max_tiles, cudaStream_t s) {
+  auto kern = k_grouped_gemm_pair<SWIGLU>;
+  static bool attr = false;
+  if (!attr) {
+    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM));
+    attr = true;
+  }
+  long long pairs = sm_count() / 2;
+  if (max_tiles < pairs) pairs = max_tiles < 1 ? 1 : max_tiles;
+  kern<<<(int)(2 * pairs), NUM_THREADS, P_SMEM, s>>>(ma, mb, md, a);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+static int pair_mode() {
+  static const int v = [] {
+    const char* e = getenv("MX_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 }  // namespace gemm
 
 int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,
@@ -597,6 +892,16 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
     if (bn == 256) return swiglu ? launch<256, true, true>(ma, mb, md, a, max_tiles, s)
                                  : launch<256, false, true>(ma, mb, md, a, max_tiles, s);
     return launch<128, false, true>(ma, mb, md, a, max_tiles, s);
+  }
+  if (bn == 256 && out_dtype == MX_BF16 && pair_mode()) {
+    // CTA-pair kernel: A box 128 rows (each CTA its half of the 256-row tile),
+    // B box 128 rows (each CTA half of the 256 output columns)
+    CUtensorMap mb2;
+    rc = make_map(&mb2, B, b_rows, K, 128);
+    if (rc) return rc;
+    const long long pair_tiles = ((M_total + 255) / 256 + G) * (N / 256);
+    return swiglu ? launch_pair<true>(ma, mb2, md, a, pair_tiles, s)
+                  : launch_pair<false>(ma, mb2, md, a, pair_tiles, s);
   }
   if (bn == 256) return swiglu ? launch<256, true, false>(ma, mb, md, a, max_tiles, s)
                                : launch<256, false, false>(ma, mb, md, a, max_tiles, s);
