@@ -30,7 +30,8 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;   // bf16 elements per k-block: 128 B rows, one SWIZZLE_128B atom wide
 constexpr int BKB = 128; // bytes per k-block row (64 bf16 or 128 e4m3)
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 256;      // CTA-pair kernel: 4 epilogue warps
+constexpr int NUM_THREADS_1 = 384;    // single-CTA kernel: warps 4..11 = 8 epilogue warps
 
 template <int BN>
 struct Cfg {
@@ -39,7 +40,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BKB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
-  static constexpr int STAGING = 4 * 2 * 32 * 64;  // per epilogue warp: 2 x (32 rows x 64 B)
+  static constexpr int STAGING = 8 * 32 * 64;  // per epilogue warp: 32 rows x 64 B
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + STAGING;
 };
 
@@ -178,6 +179,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 __device__ __forceinline__ void tma_store_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
+__device__ __forceinline__ void tma_store_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -186,10 +190,14 @@ __device__ __forceinline__ void tma_store_wait_all() {
 // SWIZZLE_64B layout the D tensor map expects (16 B chunk j of row r lives
 // at chunk j ^ ((r >> 1) & 3)), then one lane TMA-stores the 32x32 box.
 // Rows are complete boxes only; partial boxes use direct stores.
+template <int PENDING>  // 1: double-buffered staging, 0: single buffer
 __device__ __forceinline__ void stage_store_chunk(unsigned char* stg, const uint32_t (&p)[16],
                                                   int lane, const CUtensorMap* map, int col,
                                                   int row0) {
-  if (lane == 0) tma_store_wait_read1();  // this buffer's previous store has been read
+  if (lane == 0) {  // this buffer's previous store has been read out of smem
+    if constexpr (PENDING == 1) tma_store_wait_read1();
+    else tma_store_wait_read0();
+  }
   __syncwarp();
   unsigned char* rowp = stg + lane * 64;
 #pragma unroll
@@ -232,7 +240,7 @@ __device__ __forceinline__ void decode_tile(int t, const int* s_tstart, int G, i
 }
 
 template <int BN, bool SWIGLU, bool GATHER, bool FP8>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS_1, 1)
 k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
                const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_d, Args args) {
@@ -291,7 +299,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -387,11 +395,13 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue: thread = accumulator row (TMEM lane)
+    // ===== epilogue: thread = accumulator row (TMEM lane); two warps per lane
+    // quarter split the tile's columns (warps 4-7: first half, 8-11: second)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
-    unsigned char* my_stage = staging + q * (2 * 32 * 64);
-    int buf = 0;
+    unsigned char* my_stage = staging + (warp - 4) * (32 * 64);
+    constexpr int buf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
@@ -418,7 +428,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         // tile columns [0, BN/2) = gate, [BN/2, BN) = up (w13 interleave)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.D) + row * args.ldd + nb * (BN / 2);
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
+        for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
           uint32_t gr[32], ur[32];
           tmem_ld32(tbase + c, gr);
           tmem_ld32(tbase + BN / 2 + c, ur);
@@ -436,8 +446,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
             packed[i] = *reinterpret_cast<uint32_t*>(&b2);
           }
           if (full_box) {
-            stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * (BN / 2) + c, row0);
-            buf ^= 1;
+            stage_store_chunk<0>(my_stage + buf * 2048, packed, lane, &map_d, nb * (BN / 2) + c, row0);
           } else if (valid) {
             uint4* dst = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
@@ -447,7 +456,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
           uint32_t r[32];
           tmem_ld32(tbase + c, r);
           tmem_wait_ld();
@@ -470,8 +479,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
               packed[i] = *reinterpret_cast<uint32_t*>(&b2);
             }
             if (full_box) {
-              stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * BN + c, row0);
-              buf ^= 1;
+              stage_store_chunk<0>(my_stage + buf * 2048, packed, lane, &map_d, nb * BN + c, row0);
             } else if (valid) {
               uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.D) +
                                                     row * args.ldd + nb * BN + c);
@@ -718,7 +726,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
             packed[i] = *reinterpret_cast<uint32_t*>(&b2);
           }
           if (full_box) {
-            stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * (BN / 2) + c, row0);
+            stage_store_chunk<1>(my_stage + buf * 2048, packed, lane, &map_d, nb * (BN / 2) + c, row0);
             buf ^= 1;
           } else if (valid) {
             uint4* dst = reinterpret_cast<uint4*>(out + c);
@@ -741,7 +749,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
             packed[i] = *reinterpret_cast<uint32_t*>(&b2);
           }
           if (full_box) {
-            stage_store_chunk(my_stage + buf * 2048, packed, lane, &map_d, nb * BN + c, row0);
+            stage_store_chunk<1>(my_stage + buf * 2048, packed, lane, &map_d, nb * BN + c, row0);
             buf ^= 1;
           } else if (valid) {
             uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.D) +
@@ -826,7 +834,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   }
   long long grid = sm_count();
   if (max_tiles < grid) grid = max_tiles < 1 ? 1 : max_tiles;
-  kern<<<(int)grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ma, mb, md, a);
+  kern<<<(int)grid, NUM_THREADS_1, Cfg<BN>::SMEM, s>>>(ma, mb, md, a);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -847,12 +855,20 @@ static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   return MX_OK;
 }
 
+// 0: never, 1: auto (dense single-group GEMMs, e.g. the shared expert),
+// 2: always.  Measured (tools/gemm_bench.py): the pair kernel wins on dense
+// shapes (1580 vs 1482 TF/s at 16384x4096x4096) but loses on ragged experts
+// (256-row tiles pad ~25% of 512+-22-row experts vs ~12% with 128 rows).
 static int pair_mode() {
   static const int v = [] {
     const char* e = getenv("MX_GEMM_PAIR");
     return e ? atoi(e) : 1;
   }();
   return v;
+}
+static bool use_pair(int G, long long M_total) {
+  const int mode = pair_mode();
+  return mode == 2 || (mode == 1 && G == 1 && M_total >= 512);
 }
 
 }  // namespace gemm
@@ -893,7 +909,7 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
                                  : launch<256, false, true>(ma, mb, md, a, max_tiles, s);
     return launch<128, false, true>(ma, mb, md, a, max_tiles, s);
   }
-  if (bn == 256 && out_dtype == MX_BF16 && pair_mode()) {
+  if (bn == 256 && out_dtype == MX_BF16 && use_pair(G, M_total)) {
     // CTA-pair kernel: A box 128 rows (each CTA its half of the 256-row tile),
     // B box 128 rows (each CTA half of the 256 output columns)
     CUtensorMap mb2;
