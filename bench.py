@@ -485,6 +485,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tp", type=int, default=None)
+    ap.add_argument("--tokens", type=int, default=None,
+                    help="override the global token count (default 8192, BASELINE configs[1])")
     ap.add_argument("--wire", default="auto", choices=["auto", "slot", "token"],
                     help="auto: token (dedup dispatch, pre-reduced combine) when n > 1")
     ap.add_argument("--no-cpu", action="store_true")
@@ -492,6 +494,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=512)
     ap.add_argument("--ref-sample", type=int, default=512)
     args = ap.parse_args()
+    if args.tokens:
+        global T_GLOBAL
+        T_GLOBAL = args.tokens
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
