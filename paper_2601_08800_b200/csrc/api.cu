@@ -34,6 +34,8 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 // One thread per peer.  A watchdog turns a lost peer into an error flag
 // instead of a hang (SURVEY.md §5 failure detection).
 __global__ void k_barrier(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) {
     // epochs live on the device so the barrier can be replayed in a CUDA graph;
@@ -62,7 +64,7 @@ __global__ void k_barrier(DevView v) {
 }
 
 int launch_barrier(const DevView& v, cudaStream_t s) {
-  k_barrier<<<1, 64, 0, s>>>(v);
+  pdl_launch(k_barrier, 1, 64, 0, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }

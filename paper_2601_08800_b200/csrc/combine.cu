@@ -21,6 +21,8 @@ namespace mx {
 // vector is issued before any is consumed (KU x 16 B in flight per lane).
 template <int DT, bool VEC, int KU>
 __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = VEC ? Elt<DT>::V : 1;  // elements per 16 B vector
@@ -181,9 +183,9 @@ static void launch_combine_dt(const DevView& v, int blocks, cudaStream_t s) {
   col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
   const bool vec = ((size_t)c0 * v.elt) % 16 == 0 && ((size_t)(c1 - c0) * v.elt) % 16 == 0 &&
                    ((size_t)v.h * v.elt) % 16 == 0;
-  if (vec && v.k <= 8 && v.m <= 8) k_combine<DT, true, 8><<<blocks, 256, 0, s>>>(v);
-  else if (vec) k_combine<DT, true, 0><<<blocks, 256, 0, s>>>(v);
-  else k_combine<DT, false, 0><<<blocks, 256, 0, s>>>(v);
+  if (vec && v.k <= 8 && v.m <= 8) pdl_launch(k_combine<DT, true, 8>, blocks, 256, 0, s, v);
+  else if (vec) pdl_launch(k_combine<DT, true, 0>, blocks, 256, 0, s, v);
+  else pdl_launch(k_combine<DT, false, 0>, blocks, 256, 0, s, v);
 }
 
 int launch_combine(const DevView& v, cudaStream_t s) {

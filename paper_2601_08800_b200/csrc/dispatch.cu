@@ -48,6 +48,8 @@ __device__ __forceinline__ void warp_copy(char* dst, const char* src, size_t nby
 }
 
 __global__ void __launch_bounds__(256) k_dispatch(DevView v, const char* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -85,7 +87,7 @@ int launch_dispatch(const DevView& v, const void* x, cudaStream_t s) {
   if (total == 0) return MX_OK;
   long long blocks = (total + 7) / 8;  // 8 warps per CTA, one slot per warp
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_dispatch<<<(int)blocks, 256, 0, s>>>(v, static_cast<const char*>(x));
+  pdl_launch(k_dispatch, (int)blocks, 256, 0, s, v, static_cast<const char*>(x));
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -94,6 +96,8 @@ int launch_dispatch(const DevView& v, const void* x, cudaStream_t s) {
 // the expert-major RECV the grouped GEMM gathers them straight from x; this
 // kernel only writes the row table recv_src[p] = token of slot p.
 __global__ void k_rowsrc_slot(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
   int* src = at<int>(v, v.rank, v.off.recv_src);
   const long long total = (long long)v.T * v.k;
@@ -109,7 +113,7 @@ int launch_rowsrc_slot(const DevView& v, cudaStream_t s) {
   if (total == 0) return MX_OK;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_rowsrc_slot<<<(int)blocks, 256, 0, s>>>(v);
+  pdl_launch(k_rowsrc_slot, (int)blocks, 256, 0, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }

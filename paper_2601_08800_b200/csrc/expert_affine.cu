@@ -13,6 +13,8 @@ template <int DT>
 __global__ void __launch_bounds__(256)
 k_expert_affine(DevView v, const typename Elt<DT>::Acc* __restrict__ scales,
                 const typename Elt<DT>::Acc* __restrict__ biases) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   __shared__ int s_off[MX_EMAX + 1];
@@ -52,15 +54,15 @@ int launch_expert_affine(const DevView& v, const void* scales, const void* biase
   if (blocks > 148 * 8) blocks = 148 * 8;
   switch (v.elt) {
     case 8:
-      k_expert_affine<MX_F64><<<(int)blocks, 256, 0, s>>>(
+      pdl_launch(k_expert_affine<MX_F64>, (int)blocks, 256, 0, s, 
           v, static_cast<const double*>(scales), static_cast<const double*>(biases));
       break;
     case 4:
-      k_expert_affine<MX_F32><<<(int)blocks, 256, 0, s>>>(
+      pdl_launch(k_expert_affine<MX_F32>, (int)blocks, 256, 0, s, 
           v, static_cast<const float*>(scales), static_cast<const float*>(biases));
       break;
     default:
-      k_expert_affine<MX_BF16><<<(int)blocks, 256, 0, s>>>(
+      pdl_launch(k_expert_affine<MX_BF16>, (int)blocks, 256, 0, s, 
           v, static_cast<const float*>(scales), static_cast<const float*>(biases));
   }
   MX_LAUNCH_CHECK();

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(NUM_THREADS_1, 1)
 k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
                const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_d, Args args) {
+  pdl_trigger();
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -266,6 +267,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
 
   // group offsets/counts -> smem (parallel loads), then the per-group tile
   // prefix by one warp-scan pass (G <= MX_EMAX); no per-tile global reads
+  pdl_wait();  // group offsets/counts and A are written by earlier kernels
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     s_off[g] = args.offs[g];
     s_cnt[g] = args.cnts[g];
@@ -569,6 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_d, Args args) {
+  pdl_trigger();
   constexpr int BN = 256, PM = 256;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -591,6 +594,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
   const int G = args.G, nN = args.N / BN, kblocks = args.K / BK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
+  pdl_wait();  // group offsets/counts and A are written by earlier kernels
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     s_off[g] = args.offs[g];
     s_cnt[g] = args.cnts[g];
@@ -834,7 +838,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   }
   long long grid = sm_count();
   if (max_tiles < grid) grid = max_tiles < 1 ? 1 : max_tiles;
-  kern<<<(int)grid, NUM_THREADS_1, Cfg<BN>::SMEM, s>>>(ma, mb, md, a);
+  pdl_launch(kern, (int)grid, NUM_THREADS_1, Cfg<BN>::SMEM, s, ma, mb, md, a);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -850,7 +854,7 @@ static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   }
   long long pairs = sm_count() / 2;
   if (max_tiles < pairs) pairs = max_tiles < 1 ? 1 : max_tiles;
-  kern<<<(int)(2 * pairs), NUM_THREADS, P_SMEM, s>>>(ma, mb, md, a);
+  pdl_launch(kern, (int)(2 * pairs), NUM_THREADS, P_SMEM, s, ma, mb, md, a);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }

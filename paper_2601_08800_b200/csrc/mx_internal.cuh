@@ -142,6 +142,31 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
                "r"(v.z), "r"(v.w) : "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: every kernel of the layer is launched with
+// programmatic stream serialisation, triggers its dependents at entry and
+// waits (griddepcontrol.wait) before reading its predecessor's outputs, so a
+// kernel's launch and prologue overlap the previous kernel's tail (also
+// inside the captured CUDA graph).  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- dtypes
 template <int DT> struct Elt;
 template <> struct Elt<MX_F64> { using T = double; using Acc = double; static constexpr int V = 2; };

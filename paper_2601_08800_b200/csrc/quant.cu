@@ -13,6 +13,8 @@ namespace mx {
 __global__ void __launch_bounds__(256)
 k_quant_rows(const __nv_bfloat16* __restrict__ src, long long lds, unsigned char* __restrict__ dst,
              long long ldd, long long rows, const int32_t* rows_dev, int cols) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -52,7 +54,7 @@ int quant_rows_e4m3(const void* src, long long lds, void* dst, long long ldd, lo
   long long blocks = (rows + 7) / 8;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_quant_rows<<<(int)blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src), lds,
+  pdl_launch(k_quant_rows, (int)blocks, 256, 0, s, static_cast<const __nv_bfloat16*>(src), lds,
                                             static_cast<unsigned char*>(dst), ldd, rows, rows_dev,
                                             cols);
   MX_LAUNCH_CHECK();

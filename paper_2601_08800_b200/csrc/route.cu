@@ -26,6 +26,8 @@ namespace mx {
 template <class WT, int EV>
 __global__ void __launch_bounds__(256)
 k_gate(DevView v, const float* __restrict__ logits) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (tok >= v.T) return;
@@ -107,6 +109,8 @@ template <class WT>
 __global__ void __launch_bounds__(512)
 k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__ ids_in,
         const WT* __restrict__ w_in) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = v.T, E = v.E, k = v.k, n = v.n;
   const int c = blockIdx.x, t0 = c * MX_CHUNK;
@@ -231,6 +235,8 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
 // coalesced over the expert-major [E][C] layout; publishes the group's
 // per-expert totals into every rank's count matrix (peer stores in SPMD).
 __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int E = v.E, n = v.n, C = v.C;
@@ -271,6 +277,8 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
 // then the grid writes every slot's expert-major row and token-major index
 // and every (token, host) pair row.
 __global__ void __launch_bounds__(512) k_layout(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   extern __shared__ int sm[];
   const int n = v.n, E = v.E, k = v.k, j = v.group;
   int* s_cnt = sm;                   // [n][E]
@@ -404,7 +412,7 @@ __global__ void __launch_bounds__(512) k_layout(DevView v) {
 
 template <class WT, int EV>
 static void launch_gate_ev(const DevView& v, const float* logits, cudaStream_t s) {
-  k_gate<WT, EV><<<(v.T + 7) / 8, 256, 0, s>>>(v, logits);
+  pdl_launch(k_gate<WT, EV>, (v.T + 7) / 8, 256, 0, s, v, logits);
 }
 
 template <class WT>
@@ -422,7 +430,7 @@ static int launch_route_wt(const DevView& v, int C, size_t smem, const float* lo
     MX_CUDA(cudaFuncSetAttribute(k_route<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  k_route<WT><<<C, 512, smem, s>>>(v, logits, ids, static_cast<const WT*>(w));
+  pdl_launch(k_route<WT>, C, 512, smem, s, v, logits, ids, static_cast<const WT*>(w));
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -437,7 +445,7 @@ int launch_route(const DevView& v, const float* logits, const int32_t* ids,
                       : launch_route_wt<float>(v, C, smem, logits, ids, w, s);
   if (rc) return rc;
   const int warps = v.E + 2 * v.n;
-  k_route_scan<<<(warps + 7) / 8, 256, 0, s>>>(v);
+  pdl_launch(k_route_scan, (warps + 7) / 8, 256, 0, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -454,7 +462,7 @@ int launch_layout(const DevView& v, cudaStream_t s) {
   long long blocks = (work + 511) / 512;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 2) blocks = 148 * 2;
-  k_layout<<<(int)blocks, 512, smem, s>>>(v);
+  pdl_launch(k_layout, (int)blocks, 512, smem, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }

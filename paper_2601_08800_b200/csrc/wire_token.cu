@@ -44,6 +44,8 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 // peer on that host: the pair's packed (slot row, weight) list and its length.
 template <class WT>
 __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -106,6 +108,8 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
 // stored to every slot row of the pair.
 template <class WT>
 __global__ void __launch_bounds__(256) k_expand(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -131,6 +135,8 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
 // all slot loads of a column vector are issued before use (KU in flight).
 template <int DT, class WT>
 __global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
@@ -191,6 +197,8 @@ __global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
 // (ascending) of z; then push the shard to every TP rank of the group.
 template <int DT>
 __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
@@ -246,6 +254,8 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
 // recv_src[p] = u for every slot row p of pair u.
 template <class WT>
 __global__ void k_rowsrc_token(DevView v) {
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs are visible after this
   const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
@@ -281,15 +291,15 @@ int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s) {
   int rc = check_vec(v);
   if (rc) return rc;
   if (v.T == 0) return MX_OK;
-  if (v.elt == 8) k_dispatch_token<double><<<blocks_for(v.T), 256, 0, s>>>(v, static_cast<const char*>(x));
-  else k_dispatch_token<float><<<blocks_for(v.T), 256, 0, s>>>(v, static_cast<const char*>(x));
+  if (v.elt == 8) pdl_launch(k_dispatch_token<double>, blocks_for(v.T), 256, 0, s, v, static_cast<const char*>(x));
+  else pdl_launch(k_dispatch_token<float>, blocks_for(v.T), 256, 0, s, v, static_cast<const char*>(x));
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
 
 int launch_expand(const DevView& v, cudaStream_t s) {
-  if (v.elt == 8) k_expand<double><<<blocks_for((long long)v.T * v.n), 256, 0, s>>>(v);
-  else k_expand<float><<<blocks_for((long long)v.T * v.n), 256, 0, s>>>(v);
+  if (v.elt == 8) pdl_launch(k_expand<double>, blocks_for((long long)v.T * v.n), 256, 0, s, v);
+  else pdl_launch(k_expand<float>, blocks_for((long long)v.T * v.n), 256, 0, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -298,8 +308,8 @@ int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
   long long blocks = ((long long)v.T * v.n * v.KH + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  if (v.elt == 8) k_rowsrc_token<double><<<(int)blocks, 256, 0, s>>>(v);
-  else k_rowsrc_token<float><<<(int)blocks, 256, 0, s>>>(v);
+  if (v.elt == 8) pdl_launch(k_rowsrc_token<double>, (int)blocks, 256, 0, s, v);
+  else pdl_launch(k_rowsrc_token<float>, (int)blocks, 256, 0, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -307,9 +317,9 @@ int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
 int launch_pair_reduce(const DevView& v, cudaStream_t s) {
   const int g = blocks_for((long long)v.T * v.n);
   switch (v.elt) {
-    case 8: k_pair_reduce<MX_F64, double><<<g, 256, 0, s>>>(v); break;
-    case 4: k_pair_reduce<MX_F32, float><<<g, 256, 0, s>>>(v); break;
-    default: k_pair_reduce<MX_BF16, float><<<g, 256, 0, s>>>(v);
+    case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, 256, 0, s, v); break;
+    case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, 256, 0, s, v); break;
+    default: pdl_launch(k_pair_reduce<MX_BF16, float>, g, 256, 0, s, v);
   }
   MX_LAUNCH_CHECK();
   return MX_OK;
@@ -321,9 +331,9 @@ int launch_combine_token(const DevView& v, cudaStream_t s) {
   if (v.T == 0) return MX_OK;
   const int g = blocks_for(v.T);
   switch (v.elt) {
-    case 8: k_combine_token<MX_F64><<<g, 256, 0, s>>>(v); break;
-    case 4: k_combine_token<MX_F32><<<g, 256, 0, s>>>(v); break;
-    default: k_combine_token<MX_BF16><<<g, 256, 0, s>>>(v);
+    case 8: pdl_launch(k_combine_token<MX_F64>, g, 256, 0, s, v); break;
+    case 4: pdl_launch(k_combine_token<MX_F32>, g, 256, 0, s, v); break;
+    default: pdl_launch(k_combine_token<MX_BF16>, g, 256, 0, s, v);
   }
   MX_LAUNCH_CHECK();
   return MX_OK;
