@@ -34,7 +34,6 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 // One thread per peer.  A watchdog turns a lost peer into an error flag
 // instead of a hang (SURVEY.md §5 failure detection).
 __global__ void k_barrier(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) {

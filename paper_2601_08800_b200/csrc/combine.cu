@@ -21,7 +21,6 @@ namespace mx {
 // vector is issued before any is consumed (KU x 16 B in flight per lane).
 template <int DT, bool VEC, int KU>
 __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;

@@ -48,7 +48,6 @@ __device__ __forceinline__ void warp_copy(char* dst, const char* src, size_t nby
 }
 
 __global__ void __launch_bounds__(256) k_dispatch(DevView v, const char* __restrict__ x) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -96,7 +95,6 @@ int launch_dispatch(const DevView& v, const void* x, cudaStream_t s) {
 // the expert-major RECV the grouped GEMM gathers them straight from x; this
 // kernel only writes the row table recv_src[p] = token of slot p.
 __global__ void k_rowsrc_slot(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
   int* src = at<int>(v, v.rank, v.off.recv_src);

@@ -13,7 +13,6 @@ template <int DT>
 __global__ void __launch_bounds__(256)
 k_expert_affine(DevView v, const typename Elt<DT>::Acc* __restrict__ scales,
                 const typename Elt<DT>::Acc* __restrict__ biases) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;

@@ -144,10 +144,12 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
 
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: every kernel of the layer is launched with
-// programmatic stream serialisation, triggers its dependents at entry and
-// waits (griddepcontrol.wait) before reading its predecessor's outputs, so a
-// kernel's launch and prologue overlap the previous kernel's tail (also
-// inside the captured CUDA graph).  Without the attribute both are no-ops.
+// programmatic stream serialisation and waits (griddepcontrol.wait) before
+// reading its predecessor's outputs; dependents are released as each CTA
+// exits (implicit trigger), so a kernel's launch and prologue overlap the
+// previous kernel's tail (also inside the captured CUDA graph).  An explicit
+// trigger at entry was measured to hurt: the persistent GEMM's early CTAs
+// squat registers while the multi-wave dispatch is still running.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

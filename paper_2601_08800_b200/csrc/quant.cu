@@ -13,7 +13,6 @@ namespace mx {
 __global__ void __launch_bounds__(256)
 k_quant_rows(const __nv_bfloat16* __restrict__ src, long long lds, unsigned char* __restrict__ dst,
              long long ldd, long long rows, const int32_t* rows_dev, int cols) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;

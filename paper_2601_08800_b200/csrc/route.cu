@@ -26,7 +26,6 @@ namespace mx {
 template <class WT, int EV>
 __global__ void __launch_bounds__(256)
 k_gate(DevView v, const float* __restrict__ logits) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -109,7 +108,6 @@ template <class WT>
 __global__ void __launch_bounds__(512)
 k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__ ids_in,
         const WT* __restrict__ w_in) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = v.T, E = v.E, k = v.k, n = v.n;
@@ -235,7 +233,6 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
 // coalesced over the expert-major [E][C] layout; publishes the group's
 // per-expert totals into every rank's count matrix (peer stores in SPMD).
 __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -277,7 +274,6 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
 // then the grid writes every slot's expert-major row and token-major index
 // and every (token, host) pair row.
 __global__ void __launch_bounds__(512) k_layout(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   extern __shared__ int sm[];
   const int n = v.n, E = v.E, k = v.k, j = v.group;

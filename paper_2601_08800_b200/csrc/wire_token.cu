@@ -44,7 +44,6 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 // peer on that host: the pair's packed (slot row, weight) list and its length.
 template <class WT>
 __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* __restrict__ x) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -108,7 +107,6 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
 // stored to every slot row of the pair.
 template <class WT>
 __global__ void __launch_bounds__(256) k_expand(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -135,7 +133,6 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
 // all slot loads of a column vector are issued before use (KU in flight).
 template <int DT, class WT>
 __global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
@@ -197,7 +194,6 @@ __global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
 // (ascending) of z; then push the shard to every TP rank of the group.
 template <int DT>
 __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
@@ -254,7 +250,6 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
 // recv_src[p] = u for every slot row p of pair u.
 template <class WT>
 __global__ void k_rowsrc_token(DevView v) {
-  pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
