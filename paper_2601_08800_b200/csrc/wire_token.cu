@@ -122,7 +122,18 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
     int rows[MX_KMAX];
     for (int i = 0; i < cnt; ++i) rows[i] = pe[u * v.KH + i].p;
     const char* src = xbuf + (size_t)u * row_bytes;
-    for (size_t o = (size_t)lane * 16; o < row_bytes; o += 512) {
+    size_t o = (size_t)lane * 16;
+    for (; o + 3 * 512 < row_bytes; o += 4 * 512) {  // 4 x 16 B loads in flight per lane
+      uint4 val[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) val[q] = ld_v4(src + o + q * 512);
+      for (int i = 0; i < cnt; ++i) {
+        char* dst = recv + (size_t)rows[i] * row_bytes + o;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st_v4(dst + q * 512, val[q]);
+      }
+    }
+    for (; o < row_bytes; o += 512) {
       const uint4 val = ld_v4(src + o);
       for (int i = 0; i < cnt; ++i) st_v4(recv + (size_t)rows[i] * row_bytes + o, val);
     }
@@ -132,7 +143,7 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
 // z[u] = sum over the pair's slots (experts ascending) of w * partial[p];
 // all slot loads of a column vector are issued before use (KU in flight).
 template <int DT, class WT>
-__global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
+__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
@@ -157,30 +168,45 @@ __global__ void __launch_bounds__(256) k_pair_reduce(DevView v) {
       rp[i] = part + (size_t)e.p * h;
       w[i] = (A)e.w;
     }
-    for (int c = lane * V; c < h; c += 32 * V) {
-      A acc[V];
-#pragma unroll
-      for (int q = 0; q < V; ++q) acc[q] = (A)0;
-      if (cnt <= KU) {
-        uint4 raw[KU];
-#pragma unroll
-        for (int i = 0; i < KU; ++i)
-          if (i < cnt) raw[i] = ld_v4(rp[i] + c);
+    int c = lane * V;
+    if (cnt <= KU) {
+      for (; c + 32 * V < h; c += 64 * V) {  // two column vectors per lane: 2 x cnt loads in flight
+        uint4 raw[2][KU];
 #pragma unroll
         for (int i = 0; i < KU; ++i)
           if (i < cnt) {
-            const T* pv = reinterpret_cast<const T*>(&raw[i]);
-#pragma unroll
-            for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+            raw[0][i] = ld_v4(rp[i] + c);
+            raw[1][i] = ld_v4(rp[i] + c + 32 * V);
           }
-      } else {
-        for (int i = 0; i < cnt; ++i) {
-          const PairEnt<WT> e = pe[u * v.KH + i];
-          const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
-          const T* pv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-          for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
+        for (int hh = 0; hh < 2; ++hh) {
+          A acc[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = (A)0;
+#pragma unroll
+          for (int i = 0; i < KU; ++i)
+            if (i < cnt) {
+              const T* pv = reinterpret_cast<const T*>(&raw[hh][i]);
+#pragma unroll
+              for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+            }
+          T out[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+          st_v4(z + (size_t)u * h + c + hh * 32 * V, *reinterpret_cast<uint4*>(out));
         }
+      }
+    }
+    for (; c < h; c += 32 * V) {
+      A acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = (A)0;
+      for (int i = 0; i < cnt; ++i) {
+        const PairEnt<WT> e = pe[u * v.KH + i];
+        const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+        const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
       }
       T out[V];
 #pragma unroll
