@@ -213,14 +213,15 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
     model = {}
     model["route"] = {"bound": "hbm", "bytes": T * E * 4 + slots * 16 + E * 4}
     if n * m == 1:
-        model["dispatch"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
+        # x read once (slot rows re-read from L2), expert-major rows written
+        model["dispatch"] = {"bound": "hbm", "bytes": T * hb + S_d * hb}
         model["combine"] = {"bound": "hbm", "bytes": slots * hb + T * hb}
     else:
         if remote_in > 0:
             model["dispatch"] = {"bound": "nvlink", "bytes": remote_in * hb,
                                  "local_hbm_bytes": 2 * local_rows * hb}
         else:   # one group (pure TP): every row is a local gather
-            model["dispatch"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
+            model["dispatch"] = {"bound": "hbm", "bytes": T * hb + S_d * hb}
         # pulls: every slot's column shard from the m TP ranks of its host,
         # minus the one local read; plus the (m-1)/m of y pushed by TP peers
         own_host_slots = int(S[group, group])
@@ -231,8 +232,8 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
         U = np.asarray(U, dtype=np.int64)
         remote_pairs = int(U[:, group].sum() - U[group, group])
         model["dispatch"] = {"bound": "nvlink", "bytes": remote_pairs * hb}
-        model["expand"] = {"bound": "hbm", "bytes": 2 * S_d * hb}
         pairs_host = int(U[:, group].sum())
+        model["expand"] = {"bound": "hbm", "bytes": pairs_host * hb + S_d * hb}
         model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * hb + pairs_host * hb}
         pull = (int(U[group].sum()) * m - int(U[group, group])) * (H // m) * 2
         model["combine"] = {"bound": "nvlink", "bytes": pull + T * H * (m - 1) // m * 2}
@@ -438,9 +439,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(sample_tokens=args.cpu_sample)
 
-    # gate, route, scan, meta, slotpos, dispatch, gemm1, gemm2, combine (+4 barriers;
-    # +expand, +pair_reduce for wire TOKEN)
-    launches_per_step = 9 + (4 if world > 1 else 0) + (2 if wire == "token" else 0)
+    # gate, route, scan, layout, dispatch, gemm1, gemm2, combine (+4 barriers;
+    # +expand, +pair_reduce for wire TOKEN) -- profiles/r01b_n1_launches.csv
+    launches_per_step = 8 + (4 if world > 1 else 0) + (2 if wire == "token" else 0)
     if rank == 0:
         line = {
             "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",
