@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MX_ABI_VERSION 1
+#define MX_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define MX_API __attribute__((visibility("default")))
@@ -59,6 +59,16 @@ typedef enum { MX_EXPERT_AFFINE = 0, MX_EXPERT_SWIGLU = 1, MX_EXPERT_SWIGLU_FP8 
  * (token, host) before the pull; the routing tables and
  * send/recv slot lists are identical, only the bytes on NVLink shrink.   */
 typedef enum { MX_WIRE_SLOT = 0, MX_WIRE_TOKEN = 1 } mx_wire;
+
+/* Gate applied by mx_route when it is given logits.
+ * SOFTMAX: Qwen3-MoE -- fp32 softmax over E, top-k by logit, optional
+ *   renormalisation (transformers modeling_qwen3_moe.py router).
+ * GROUP_LIMITED: DeepSeek-V3 -- sigmoid scores, key = score + correction
+ *   bias, top-2-sum group scores, keep router_topk_groups of router_groups,
+ *   top-k of the masked key, weights = score (/ (sum + 1e-20) when
+ *   renormalize) * routed_scaling (transformers modeling_deepseek_v3.py
+ *   DeepseekV3MoE.route_tokens_to_experts).  Lowest index wins every tie. */
+typedef enum { MX_ROUTER_SOFTMAX = 0, MX_ROUTER_GROUP_LIMITED = 1 } mx_router;
 
 /* Buffers a plan exposes (for zero-copy views and parity inspection). */
 typedef enum {
@@ -96,6 +106,12 @@ typedef struct {
   int wire;           /* mx_wire                                             */
   int shared_inter;   /* shared expert intermediate size (0: none), SWIGLU_FP8 */
   long long capacity; /* receive rows per host; <=0: worst case T*n*min(k,E/n+1) */
+  /* gate (zero-initialised: SOFTMAX) */
+  int router;              /* mx_router                                      */
+  int router_groups;       /* GROUP_LIMITED: expert groups (E % groups == 0) */
+  int router_topk_groups;  /* GROUP_LIMITED: groups kept per token           */
+  float routed_scaling;    /* GROUP_LIMITED: weight scale (0 -> 1.0)         */
+  const float* router_bias;/* GROUP_LIMITED: [E] fp32 device, may be NULL    */
 } mx_plan_desc;
 
 /* Expert parameters for one rank (device pointers). */

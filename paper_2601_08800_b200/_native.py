@@ -25,6 +25,7 @@ MX_ERR_TIMEOUT = -5
 MX_F64, MX_F32, MX_BF16 = 0, 1, 2
 MX_EXPERT_AFFINE, MX_EXPERT_SWIGLU, MX_EXPERT_SWIGLU_FP8 = 0, 1, 2
 MX_WIRE_SLOT, MX_WIRE_TOKEN = 0, 1
+MX_ROUTER_SOFTMAX, MX_ROUTER_GROUP_LIMITED = 0, 1
 (MX_BUF_RECV, MX_BUF_PARTIAL, MX_BUF_Y, MX_BUF_IDS, MX_BUF_WEIGHTS,
  MX_BUF_SLOT_POS, MX_BUF_SLOT_TM, MX_BUF_CNT_ALL, MX_BUF_EXP_OFF,
  MX_BUF_EXP_CNT, MX_BUF_SEND, MX_BUF_ACT, MX_BUF_UPOS, MX_BUF_XBUF) = range(14)
@@ -40,7 +41,10 @@ class PlanDesc(C.Structure):
                 ("top_k", C.c_int), ("inter", C.c_int),
                 ("act_dtype", C.c_int), ("expert_kind", C.c_int),
                 ("renormalize", C.c_int), ("wire", C.c_int),
-                ("shared_inter", C.c_int), ("capacity", C.c_longlong)]
+                ("shared_inter", C.c_int), ("capacity", C.c_longlong),
+                ("router", C.c_int), ("router_groups", C.c_int),
+                ("router_topk_groups", C.c_int), ("routed_scaling", C.c_float),
+                ("router_bias", C.c_void_p)]
 
 
 class ExpertParams(C.Structure):

@@ -90,6 +90,17 @@ static int validate(const mx_plan_desc& d) {
   if (d.top_k > MX_KMAX) { set_error("top_k %d exceeds %d", d.top_k, MX_KMAX); return MX_ERR_UNSUPPORTED; }
   if (d.act_dtype < MX_F64 || d.act_dtype > MX_BF16) { set_error("bad act_dtype"); return MX_ERR_INVALID; }
   if (d.wire != MX_WIRE_SLOT && d.wire != MX_WIRE_TOKEN) { set_error("bad wire format"); return MX_ERR_INVALID; }
+  if (d.router == MX_ROUTER_GROUP_LIMITED) {
+    const int G = d.router_groups;
+    if (G < 1 || G > 32 || d.num_experts % G != 0 || d.num_experts / G < 2) {
+      set_error("group-limited router: groups must divide E into groups of >= 2 experts, at most 32 groups");
+      return MX_ERR_INVALID;
+    }
+    if (d.router_topk_groups < 1 || d.router_topk_groups > G) { set_error("router_topk_groups must be in [1, groups]"); return MX_ERR_INVALID; }
+    if (d.top_k > d.router_topk_groups * (d.num_experts / G)) { set_error("top_k exceeds the experts of the kept groups"); return MX_ERR_INVALID; }
+  } else if (d.router != MX_ROUTER_SOFTMAX) {
+    set_error("bad router"); return MX_ERR_INVALID;
+  }
   if (d.expert_kind == MX_EXPERT_SWIGLU_FP8) {
     if (d.act_dtype != MX_BF16) { set_error("fp8 experts take bf16 tokens"); return MX_ERR_UNSUPPORTED; }
     if (d.inter % d.tp != 0 || (d.inter / d.tp) % 128 != 0) { set_error("inter/tp must be a multiple of 128"); return MX_ERR_UNSUPPORTED; }
@@ -341,6 +352,11 @@ int mx_plan_create(mx_comm* c, const mx_plan_desc* d, mx_plan** out) {
   v.C = (d->tokens + MX_CHUNK - 1) / MX_CHUNK;
   v.elt = elt_bytes(d->act_dtype);
   v.renorm = d->renormalize;
+  v.router = d->router;
+  v.r_groups = d->router_groups;
+  v.r_topk_groups = d->router_topk_groups;
+  v.r_scaling = d->routed_scaling != 0.f ? d->routed_scaling : 1.f;
+  v.r_bias = d->router_bias;
   v.wire = d->wire;
   v.KH = kh_of(*d);
   v.fp8 = d->expert_kind == MX_EXPERT_SWIGLU_FP8;

@@ -84,6 +84,10 @@ struct DevView {
   int T, h, E, k, I_t, C;
   int elt;            // bytes per hidden element on the wire
   int renorm;
+  int router;         // mx_router: 0 softmax top-k, 1 sigmoid group-limited
+  int r_groups, r_topk_groups;  // group-limited router: groups, groups kept
+  float r_scaling;    // routed scaling factor (group-limited router)
+  const float* r_bias;  // [E] score-correction bias (device)
   int wire;           // mx_wire
   int KH;             // max slots of one token on one host
   int welt;           // bytes per element on the wire (1: e4m3)

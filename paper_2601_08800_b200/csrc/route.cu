@@ -103,6 +103,126 @@ k_gate(DevView v, const float* __restrict__ logits) {
   }
 }
 
+// DeepSeek-V3 group-limited router (transformers modeling_deepseek_v3.py
+// DeepseekV3MoE.route_tokens_to_experts), one warp per
+// token, same lane ownership as k_gate.  s = sigmoid(logit) (evaluated in
+// f64, rounded once to fp32 -- the oracle's definition), key c = s + bias;
+// group score = sum of the group's top-2 c (a warp top-2 reduction per
+// group); the r_topk_groups best groups stay (lowest group id on ties), c of
+// every other expert becomes 0.0 (masked_fill, not -inf); top-k of that key
+// (lowest id on ties); weight = s / (sum_r s_r + 1e-20) * scaling, the sum
+// running in selection order.
+template <class WT, int EV>
+__global__ void __launch_bounds__(256)
+k_gate_grouped(DevView v, const float* __restrict__ logits) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  const int lane = threadIdx.x & 31;
+  const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (tok >= v.T) return;
+  const int E = v.E, k = v.k, G = v.r_groups, gs = E / G;
+  int* ids = at<int>(v, v.rank, v.off.ids);
+  WT* w = at<WT>(v, v.rank, v.off.w);
+  const float* row = logits + (size_t)tok * E;
+  float key[EV * 4], sv[EV * 4];
+#pragma unroll
+  for (int i = 0; i < EV * 4; ++i) {
+    const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+    if (e < E) {
+      const float x = __ldg(row + e);
+      sv[i] = (float)(1.0 / (1.0 + exp(-(double)x)));
+      key[i] = __fadd_rn(sv[i], v.r_bias ? __ldg(v.r_bias + e) : 0.f);
+    } else {
+      sv[i] = 0.f;
+      key[i] = -INFINITY;
+    }
+  }
+  // group scores: top-2 sum of the choice key per group
+  unsigned keep = 0;
+  {
+    float gsc[32];
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      float m1 = -INFINITY, m2 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < EV * 4; ++i) {
+        const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+        if (e < E && e / gs == g) {
+          const float c = key[i];
+          if (c > m1) { m2 = m1; m1 = c; } else if (c > m2) { m2 = c; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float o1 = __shfl_xor_sync(0xffffffffu, m1, o);
+        const float o2 = __shfl_xor_sync(0xffffffffu, m2, o);
+        if (o1 >= m1) { m2 = fmaxf(m1, o2); m1 = o1; } else { m2 = fmaxf(m2, o1); }
+      }
+      gsc[g < 32 ? g : 31] = __fadd_rn(m1, m2);
+    }
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      int rank = 0;
+      for (int g2 = 0; g2 < G; ++g2)
+        rank += (gsc[g2] > gsc[g] || (gsc[g2] == gsc[g] && g2 < g)) ? 1 : 0;
+      if (rank < v.r_topk_groups) keep |= 1u << g;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < EV * 4; ++i) {
+    const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+    if (e < E && !((keep >> (e / gs)) & 1u)) key[i] = 0.f;
+  }
+  unsigned taken = 0;
+  float cv, cs;
+  int ce;
+  auto rescan = [&]() {
+    cv = -INFINITY;
+    cs = 0.f;
+    ce = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < EV * 4; ++i) {
+      const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+      if (e < E && !((taken >> i) & 1u) && (key[i] > cv || (key[i] == cv && e < ce))) {
+        cv = key[i];
+        cs = sv[i];
+        ce = e;
+      }
+    }
+  };
+  rescan();
+  int my_e = 0;
+  float my_s = 0.f;
+  for (int r = 0; r < k; ++r) {
+    float bv = cv;
+    int be = ce;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+    }
+    const unsigned own = __ballot_sync(0xffffffffu, be == ce);
+    const float ws = __shfl_sync(0xffffffffu, cs, __ffs(own) - 1);
+    if (lane == r) { my_e = be; my_s = ws; }
+    if (be == ce) {  // this lane owned the winner
+      taken |= 1u << (4 * (be >> 7) + (be & 3));
+      rescan();
+    }
+  }
+  float wt = my_s;
+  if (v.renorm) {
+    float den = 0.f;
+    for (int r = 0; r < k; ++r) den = __fadd_rn(den, __shfl_sync(0xffffffffu, my_s, r));
+    den = __fadd_rn(den, 1e-20f);
+    wt = __fdiv_rn(my_s, den);
+  }
+  wt = __fmul_rn(wt, v.r_scaling);
+  if (lane < k) {
+    ids[(size_t)tok * k + lane] = my_e;
+    w[(size_t)tok * k + lane] = (WT)wt;
+  }
+}
+
 // One CTA per chunk of MX_CHUNK tokens of this rank's group.
 template <class WT>
 __global__ void __launch_bounds__(512)
@@ -408,7 +528,10 @@ __global__ void __launch_bounds__(512) k_layout(DevView v) {
 
 template <class WT, int EV>
 static void launch_gate_ev(const DevView& v, const float* logits, cudaStream_t s) {
-  pdl_launch(k_gate<WT, EV>, (v.T + 7) / 8, 256, 0, s, v, logits);
+  if (v.router == MX_ROUTER_GROUP_LIMITED)
+    pdl_launch(k_gate_grouped<WT, EV>, (v.T + 7) / 8, 256, 0, s, v, logits);
+  else
+    pdl_launch(k_gate<WT, EV>, (v.T + 7) / 8, 256, 0, s, v, logits);
 }
 
 template <class WT>

@@ -40,7 +40,7 @@ class MoELayer:
                  inter, experts: SwiGLUExperts | None = None, *, rank=None,
                  w13=None, w2=None, dtype=torch.bfloat16, renormalize=True,
                  capacity=None, expert_kind="swiglu", scales=None, biases=None,
-                 process_group=None, wire="slot"):
+                 process_group=None, wire="slot", gate=None):
         self.n, self.m, self.W = n, m, n * m
         if rank is None:
             rank = dist.get_rank() if dist.is_initialized() else 0
@@ -57,7 +57,7 @@ class MoELayer:
                               inter=inter, renormalize=renormalize,
                               capacity=capacity, emulate=False, rank=rank,
                               process_group=process_group, wire=wire,
-                              shared_inter=shared_inter)
+                              shared_inter=shared_inter, gate=gate)
         self.wire = wire
         if expert_kind == "swiglu_fp8":
             self.shards = experts.rank_shard(n, m, rank)

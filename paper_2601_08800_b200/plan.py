@@ -14,6 +14,7 @@ A :class:`LayerPlan` owns one ``mx_comm`` (the symmetric heaps) and one
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 
 import torch
 
@@ -49,11 +50,34 @@ def stream_ptr(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
+@dataclass(frozen=True)
+class GateSpec:
+    """The gate ``route`` applies to logits (``mx_router`` in the C ABI).
+
+    ``softmax``: Qwen3-MoE -- softmax over E, top-k by logit (the plan's
+    ``renormalize`` renormalises over the k).  ``group_limited``:
+    DeepSeek-V3 -- sigmoid scores, correction ``bias`` [E] fp32, top-2-sum
+    group scores, ``topk_groups`` of ``groups`` kept, weights scaled by
+    ``scaling`` (transformers modeling_deepseek_v3.py
+    ``DeepseekV3MoE.route_tokens_to_experts``)."""
+
+    kind: str = "softmax"
+    groups: int = 0
+    topk_groups: int = 0
+    scaling: float = 1.0
+    bias: object = None
+
+    @classmethod
+    def deepseek_v3(cls, bias=None, groups=8, topk_groups=4, scaling=2.5):
+        return cls("group_limited", groups, topk_groups, scaling, bias)
+
+
 class LayerPlan:
     def __init__(self, n, m, tokens, hidden, num_experts, top_k, *,
                  dtype=torch.float64, expert_kind="affine", inter=0,
                  renormalize=True, capacity=None, emulate=True, rank=None,
-                 process_group=None, device=None, wire="slot", shared_inter=0):
+                 process_group=None, device=None, wire="slot", shared_inter=0,
+                 gate=None):
         lib = N.load()
         if not torch.cuda.is_available():
             raise N.NativeLibraryError("no CUDA device: the MoE layer runs "
@@ -77,6 +101,22 @@ class LayerPlan:
             1 if renormalize else 0,
             N.MX_WIRE_TOKEN if wire == "token" else N.MX_WIRE_SLOT, int(shared_inter),
             int(capacity or 0))
+        self.gate = gate or GateSpec()
+        if self.gate.kind == "group_limited":
+            self._gate_bias = None
+            if self.gate.bias is not None:
+                self._gate_bias = torch.as_tensor(self.gate.bias).to(
+                    self.device, torch.float32).contiguous()
+                if self._gate_bias.numel() != num_experts:
+                    raise StrategyError("gate bias needs one entry per expert")
+            self.desc.router = N.MX_ROUTER_GROUP_LIMITED
+            self.desc.router_groups = int(self.gate.groups)
+            self.desc.router_topk_groups = int(self.gate.topk_groups)
+            self.desc.routed_scaling = float(self.gate.scaling)
+            self.desc.router_bias = (self._gate_bias.data_ptr()
+                                     if self._gate_bias is not None else None)
+        elif self.gate.kind != "softmax":
+            raise StrategyError(f"unknown gate {self.gate.kind!r}")
         self.wire = wire
         heap = C.c_size_t()
         N.check(lib.mx_plan_heap_bytes(C.byref(self.desc), C.byref(heap)),

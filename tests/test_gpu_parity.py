@@ -208,6 +208,48 @@ def test_router_topk_bit_exact(T, E, k, renorm):
     plan.close()
 
 
+@pytest.mark.parametrize("name", ["r1", "small", "negbias"])
+def test_group_limited_router_bit_exact(name):
+    """DeepSeek-V3 gate kernel vs the oracle restatement (itself pinned to
+    transformers): ids bit-exact, weights bit-exact (same fp32 op order)."""
+    from paper_2601_08800_b200.plan import GateSpec, LayerPlan
+    z = np.load(__import__("conftest").GOLDEN / "deepseek_router.npz")
+    T, E, k, ng, tg, norm = (int(x) for x in z[f"{name}_cfg"])
+    sc = float(z[f"{name}_scaling"][0])
+    logits, bias = z[f"{name}_logits"], z[f"{name}_bias"]
+    ids_ref, w_ref = orc.router_group_limited(logits, bias, k, ng, tg, bool(norm), sc)
+    gate = GateSpec("group_limited", ng, tg, sc, torch.as_tensor(bias))
+    plan = LayerPlan(1, 1, T, 8, E, k, dtype=torch.float32, renormalize=bool(norm), gate=gate)
+    plan.route(logits=torch.as_tensor(logits).cuda())
+    plan.layout(check_capacity=True)
+    v = plan.rank_views(0)
+    assert np.array_equal(v["ids"].cpu().numpy(), ids_ref)
+    assert np.array_equal(v["weights"].cpu().numpy(), w_ref)
+    counts = np.bincount(ids_ref.reshape(-1), minlength=E)
+    assert np.array_equal(v["exp_cnt"].cpu().numpy(), counts)
+    plan.close()
+
+
+def test_group_limited_router_deepseek_shape_random():
+    """R1 shape (256 experts, 8 groups keep 4, top-8, scaling 2.5) on 4096
+    tokens with a tie row and an all-equal row."""
+    from paper_2601_08800_b200.plan import GateSpec, LayerPlan
+    rng = np.random.default_rng(5)
+    T, E, k = 4096, 256, 8
+    logits = rng.standard_normal((T, E)).astype(np.float32)
+    logits[0, :] = 0.25
+    logits[1, 7] = logits[1, 200] = 6.0
+    bias = (0.02 * rng.standard_normal(E)).astype(np.float32)
+    ids_ref, w_ref = orc.router_group_limited(logits, bias, k, 8, 4, True, 2.5)
+    plan = LayerPlan(1, 1, T, 8, E, k, dtype=torch.float32,
+                     gate=GateSpec.deepseek_v3(torch.as_tensor(bias)))
+    plan.route(logits=torch.as_tensor(logits).cuda())
+    v = plan.rank_views(0)
+    assert np.array_equal(v["ids"].cpu().numpy(), ids_ref)
+    assert np.array_equal(v["weights"].cpu().numpy(), w_ref)
+    plan.close()
+
+
 def test_router_topk_feeds_layer_2x2():
     """Gate -> table on a 2x2 cluster equals the reference fed by our gate."""
     from paper_2601_08800_b200 import build_routing_table

@@ -90,3 +90,45 @@ def test_bf16_round():
     r = orc.bf16_round(a)
     assert r[0] == 1.0 and r[1] == 1.0 and r[2] == 1.015625
     assert abs(r[3] + 3.140625) < 1e-7
+
+
+# ------------------------------------------------- DeepSeek-V3 router
+def _ds_case(name):
+    z = np.load(GOLDEN / "deepseek_router.npz")
+    T, E, k, ng, tg, norm = (int(x) for x in z[f"{name}_cfg"])
+    return z, T, E, k, ng, tg, bool(norm), float(z[f"{name}_scaling"][0])
+
+
+@pytest.mark.parametrize("name", ["r1", "small"])
+def test_group_limited_router_matches_transformers(name):
+    """Oracle vs the unmodified transformers DeepseekV3MoE router (frozen by
+    tests/golden/make_router_golden.py): ids bit-exact, weights to the fp32
+    sum-order ULPs."""
+    z, T, E, k, ng, tg, norm, sc = _ds_case(name)
+    ids, w = orc.router_group_limited(z[f"{name}_logits"], z[f"{name}_bias"], k, ng, tg,
+                                      norm, sc)
+    o = np.argsort(ids, axis=1)
+    assert np.array_equal(np.take_along_axis(ids, o, 1), z[f"{name}_ids"])
+    np.testing.assert_allclose(np.take_along_axis(w, o, 1), z[f"{name}_w"], rtol=1e-6)
+
+
+def test_group_limited_router_masked_zero_quirk():
+    """Negative choice keys: experts outside the kept groups carry 0.0
+    (masked_fill) and outrank negative kept ones, as in transformers.  Among
+    equal masked zeros torch.topk's order is unspecified (we take the lowest
+    ids), so only the strictly ranked part is compared exactly."""
+    name = "negbias"
+    z, T, E, k, ng, tg, norm, sc = _ds_case(name)
+    ids, _, key = orc.router_group_limited(z[f"{name}_logits"], z[f"{name}_bias"], k, ng,
+                                           tg, norm, sc, return_key=True)
+    ref = z[f"{name}_ids"]
+    n_exact = n_zero_rows = 0
+    for t in range(T):
+        pos = [e for e in ids[t] if key[t, e] > 0]      # strictly ranked picks
+        assert set(pos) <= set(ref[t].tolist())
+        if len(pos) == k:
+            n_exact += 1
+            assert sorted(ids[t].tolist()) == ref[t].tolist()
+        else:
+            n_zero_rows += 1
+    assert n_zero_rows > 0 and n_exact > 0
