@@ -264,7 +264,9 @@ def run_ours(args):
     w13, w2 = ex.rank_shard(n, m, rank)
     del ex
     torch.cuda.empty_cache()
-    wire = args.wire if args.wire != "auto" else ("token" if n > 1 else "slot")
+    # TOKEN wire whenever there is a peer: dedup dispatch + pair pre-reduction
+    # (for n == 1 the TP reduction then moves T rows instead of T*k slots)
+    wire = args.wire if args.wire != "auto" else ("token" if world > 1 else "slot")
     layer = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank, wire=wire)
     g = torch.Generator(device="cuda").manual_seed(1000 + group)
     x = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)

@@ -825,6 +825,18 @@ static int sm_count() {
   return n;
 }
 
+// Persistent CTAs per grouped GEMM: every SM, or MX_GEMM_CTAS when set (leaves
+// SMs free for a concurrent micro-batch's communication kernels).
+static int gemm_ctas() {
+  static int n = 0;
+  if (!n) {
+    n = sm_count();
+    const char* e = getenv("MX_GEMM_CTAS");
+    if (e && atoi(e) > 0 && atoi(e) < n) n = atoi(e);
+  }
+  return n;
+}
+
 template <int BN, bool SWIGLU, bool GATHER, bool FP8 = false>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                   const Args& a, long long max_tiles, cudaStream_t s) {
@@ -834,7 +846,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
     MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
     attr = true;
   }
-  long long grid = sm_count();
+  long long grid = gemm_ctas();
   if (max_tiles < grid) grid = max_tiles < 1 ? 1 : max_tiles;
   pdl_launch(kern, (int)grid, NUM_THREADS_1, Cfg<BN>::SMEM, s, ma, mb, md, a);
   MX_LAUNCH_CHECK();
@@ -850,7 +862,7 @@ static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
     MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM));
     attr = true;
   }
-  long long pairs = sm_count() / 2;
+  long long pairs = gemm_ctas() / 2;
   if (max_tiles < pairs) pairs = max_tiles < 1 ? 1 : max_tiles;
   pdl_launch(kern, (int)(2 * pairs), NUM_THREADS, P_SMEM, s, ma, mb, md, a);
   MX_LAUNCH_CHECK();

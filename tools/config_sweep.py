@@ -53,15 +53,17 @@ def timed(run, layer, iters, flush):
     return float(t.item())
 
 
-def layouts(world, min_tp=1):
-    return [(world // m, m) for m in (1, 2, 4, 8) if world % m == 0 and m >= min_tp]
+def layouts(world, min_tp=1, inter=None):
+    """(n, m) of every TP degree the expert shapes allow (I/m % 128 == 0)."""
+    return [(world // m, m) for m in (1, 2, 4, 8)
+            if world % m == 0 and m >= min_tp and (inter is None or (inter // m) % 128 == 0)]
 
 
 def config_c(args, rank, world, flush):
     H, I, E, K, IS = 7168, 2048, 256, 8, 2048
     out = []
     ex = FP8SwiGLUExperts.random(E, H, I, shared_inter=IS, seed=0)
-    for n, m in layouts(world, min_tp=2 if world > 1 else 1):
+    for n, m in layouts(world, min_tp=2 if world > 1 else 1, inter=I):
         T = args.tokens // n
         g = rank // m
         gen = torch.Generator(device="cuda").manual_seed(100 + g)
@@ -110,7 +112,7 @@ def config_e(args, rank, world, flush):
         res = {"config": "E", "zipf_s": s, "n_gpus": world, "global_tokens": args.tokens,
                "layouts": {}}
         counts = None
-        for n, m in layouts(world):
+        for n, m in layouts(world, inter=I):
             T = args.tokens // n
             g = rank // m
             gen = torch.Generator(device="cuda").manual_seed(100 + g)
