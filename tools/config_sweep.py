@@ -69,7 +69,7 @@ def config_c(args, rank, world, flush):
         gen = torch.Generator(device="cuda").manual_seed(100 + g)
         x = torch.randn(T, H, device="cuda", generator=gen).to(torch.bfloat16)
         logits = torch.randn(T, E, device="cuda", generator=gen)
-        wire = "token" if n > 1 else "slot"
+        wire = "token" if world > 1 else "slot"
         layer = MoELayer(n, m, T, H, E, K, I, ex, rank=rank, wire=wire)
         run = layer.capture(x, logits)
         ms = timed(run, layer, args.iters, flush)
@@ -119,7 +119,7 @@ def config_e(args, rank, world, flush):
             x = torch.randn(T, H, device="cuda", generator=gen).to(torch.bfloat16)
             logits = zipf_logits(T, E, s, seed=1, device="cuda", generator=gen)
             w13, w2 = ex.rank_shard(n, m, rank)
-            wire = "token" if n > 1 else "slot"
+            wire = "token" if world > 1 else "slot"
             layer = MoELayer(n, m, T, H, E, K, I, w13=w13, w2=w2, rank=rank, wire=wire)
             run = layer.capture(x, logits)
             ms = timed(run, layer, args.iters, flush)
