@@ -86,7 +86,8 @@ typedef enum {
   MX_BUF_ACT = 11,     /* [capacity, I/tp] bf16: SwiGLU activation           */
   MX_BUF_UPOS = 12,    /* [T, n] int32: (token, host) pair row in host's XBUF */
   MX_BUF_XBUF = 13,    /* [T*n, h] act: deduplicated rows (wire TOKEN)       */
-  MX_BUF_COUNT_ = 14
+  MX_BUF_STAMPS = 14,  /* [64] uint64: %globaltimer ns written by mx_stamp   */
+  MX_BUF_COUNT_ = 15
 } mx_buffer;
 
 typedef struct mx_comm mx_comm;
@@ -198,6 +199,11 @@ MX_API int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int
  * pushes the finished shard to every TP rank of its group (the final
  * all-gather).  y_out: optional [T, h] act copy target (NULL: MX_BUF_Y). */
 MX_API int mx_combine(mx_plan* p, int rank, void* y_out, void* stream);
+
+/* Measured-trace export: write the device clock
+ * (%globaltimer, ns) into stamp slot [0, 64) of the rank's heap, ordered
+ * after every earlier launch on the stream.  Read with MX_BUF_STAMPS.    */
+MX_API int mx_stamp(mx_plan* p, int rank, int slot, void* stream);
 /* Whole layer: route -> layout -> dispatch -> expert -> combine, with the
  * device barriers between phases in SPMD mode (run_moe_block, sim:565).  */
 MX_API int mx_forward(mx_plan* p, int rank, const void* x, const float* logits,

@@ -28,7 +28,8 @@ MX_WIRE_SLOT, MX_WIRE_TOKEN = 0, 1
 MX_ROUTER_SOFTMAX, MX_ROUTER_GROUP_LIMITED = 0, 1
 (MX_BUF_RECV, MX_BUF_PARTIAL, MX_BUF_Y, MX_BUF_IDS, MX_BUF_WEIGHTS,
  MX_BUF_SLOT_POS, MX_BUF_SLOT_TM, MX_BUF_CNT_ALL, MX_BUF_EXP_OFF,
- MX_BUF_EXP_CNT, MX_BUF_SEND, MX_BUF_ACT, MX_BUF_UPOS, MX_BUF_XBUF) = range(14)
+ MX_BUF_EXP_CNT, MX_BUF_SEND, MX_BUF_ACT, MX_BUF_UPOS, MX_BUF_XBUF,
+ MX_BUF_STAMPS) = range(15)
 
 
 class NativeLibraryError(MoeplanError, RuntimeError):
@@ -79,6 +80,7 @@ SIGNATURES = {
     "mx_expert": [VP, I, C.POINTER(ExpertParams), VP],
     "mx_expert_stage": [VP, I, C.POINTER(ExpertParams), I, VP],
     "mx_combine": [VP, I, VP, VP],
+    "mx_stamp": [VP, I, I, VP],
     "mx_forward": [VP, I, VP, VP, VP, VP, C.POINTER(ExpertParams), VP, VP],
     "mx_baseline_dispatch_pack": [VP, I, VP, VP, VP, VP],
     "mx_baseline_dispatch_unpack": [VP, I, VP, VP],

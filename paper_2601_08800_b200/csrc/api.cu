@@ -145,6 +145,7 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   o.cnt_all = take(4 * n * E);
   o.counters = take(4 * 16);
   o.err = take(4 * 16);
+  o.stamps = take(8 * MX_STAMPS);
   o.recv = take((size_t)cap * wrow);
   o.partial = take((size_t)cap * h * elt);
   o.y = take(T * h * elt);
@@ -405,6 +406,7 @@ int mx_plan_buffer(mx_plan* p, int rank, int which, void** ptr, size_t* bytes) {
     case MX_BUF_ACT: off = o.act; len = p->cap * (size_t)p->base.I_t * 2; break;
     case MX_BUF_UPOS: off = o.upos; len = 4 * T * n; break;
     case MX_BUF_XBUF: off = o.xbuf; len = (d.wire == MX_WIRE_TOKEN ? T * n : 0) * h * elt; break;
+    case MX_BUF_STAMPS: off = o.stamps; len = 8 * MX_STAMPS; break;
     default: set_error("bad buffer id %d", which); return MX_ERR_INVALID;
   }
   *ptr = p->comm->heap[rank] + off;
@@ -650,6 +652,21 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
       char* dst = static_cast<char*>(y_out) + (p->comm->emulate ? (size_t)(r / p->d.tp) * bytes : 0);
       MX_CUDA(cudaMemcpyAsync(dst, p->comm->heap[r] + p->off.y, bytes, cudaMemcpyDeviceToDevice, s));
     }
+  }
+  return MX_OK;
+}
+
+// Device timestamp (%globaltimer, ns) into the rank's stamp slot, ordered
+// after every earlier launch on the stream: the measured-trace export
+// brackets each phase with these.
+int mx_stamp(mx_plan* p, int rank, int slot, void* stream) {
+  if (slot < 0 || slot >= MX_STAMPS) { set_error("stamp slot %d outside [0, %d)", slot, MX_STAMPS); return MX_ERR_INVALID; }
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  for (int r = it.first; r < it.last; ++r) {
+    rc = launch_stamp(view_for(p, r), slot, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
   }
   return MX_OK;
 }

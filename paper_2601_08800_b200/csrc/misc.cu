@@ -148,3 +148,21 @@ int mx_dense_moe(int T, int h, int E, int k, int act_dtype, int expert_kind, int
 }
 
 }  // extern "C"
+
+namespace mx {
+
+// ---------------------------------------------------------------- stamps
+__global__ void k_stamp(DevView v, int slot) {
+  pdl_wait();  // every earlier launch on the stream has completed
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  at<unsigned long long>(v, v.rank, v.off.stamps)[slot] = t;
+}
+
+int launch_stamp(const DevView& v, int slot, cudaStream_t s) {
+  pdl_launch(k_stamp, 1, 32, 0, s, v, slot);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // namespace mx

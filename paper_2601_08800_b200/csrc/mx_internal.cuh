@@ -17,6 +17,7 @@
 #define MX_CHUNK 128       // tokens per router chunk (one CTA)
 #define MX_KMAX 32         // max top-k handled by the kernels
 #define MX_EMAX 1024       // max experts
+#define MX_STAMPS 64
 #define MX_NMAX 64         // max groups
 
 namespace mx {
@@ -76,6 +77,7 @@ struct Offsets {
   size_t sh_meta;     // int32 [4]       {0, T} offs/cnt of the shared "group"
   size_t counters;    // int32 [16]  [0]=route CTA counter [2..3]=u64 barrier epoch
   size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
+  size_t stamps;      // uint64 [MX_STAMPS] %globaltimer ns written by mx_stamp
   size_t total;
 };
 
@@ -216,6 +218,7 @@ int launch_expand(const DevView& v, cudaStream_t s);
 int launch_pair_reduce(const DevView& v, cudaStream_t s);
 int launch_combine_token(const DevView& v, cudaStream_t s);
 int launch_barrier(const DevView& v, cudaStream_t s);
+int launch_stamp(const DevView& v, int slot, cudaStream_t s);
 int launch_baseline_dispatch_pack(const DevView& v, const void* x, void* send,
                                   int32_t* counts, cudaStream_t s);
 int launch_baseline_dispatch_unpack(const DevView& v, const void* recv, cudaStream_t s);

@@ -99,10 +99,7 @@ class MoELayer:
     def forward_phases(self, x, logits, events, stream=None, event_factory=None):
         """Same launches as :meth:`forward`, phase by phase, recording a CUDA
         event after each phase (for per-kernel timing in bench.py)."""
-        p, r = self.plan, self.rank
         s = stream or torch.cuda.current_stream()
-        lib = N.load()
-        sp = stream_ptr(s)
         make = event_factory or (lambda: torch.cuda.Event(enable_timing=True))
 
         def mark(name):
@@ -110,6 +107,21 @@ class MoELayer:
             ev.record(s)
             events.append((name, ev))
 
+        return self.run_phases(x, logits, mark, s)
+
+    def phase_names(self):
+        tok = self.wire == "token"
+        return (["start", "route", "barrier_counts", "layout", "dispatch", "barrier_dispatch"]
+                + (["expand"] if tok else []) + ["gemm1_swiglu", "gemm2"]
+                + (["pair_reduce"] if tok else [])
+                + ["barrier_partials", "combine", "barrier_out"])
+
+    def run_phases(self, x, logits, mark, stream):
+        """The fused forward's launches in order, calling ``mark(phase)``
+        after each phase (and ``mark("start")`` first)."""
+        p, r, s = self.plan, self.rank, stream
+        lib = N.load()
+        sp = stream_ptr(s)
         mark("start")
         p.route(logits=logits, rank=r, stream=s); mark("route")
         p.barrier(stream=s); mark("barrier_counts")

@@ -197,6 +197,14 @@ class LayerPlan:
     def barrier(self, stream=None):
         N.check(N.load().mx_comm_barrier(self._comm, stream_ptr(stream)), "barrier")
 
+    def stamp(self, slot, rank=None, stream=None):
+        """Device clock (ns) into stamp ``slot`` after all earlier launches."""
+        N.check(N.load().mx_stamp(self._plan, self._r(rank), int(slot), stream_ptr(stream)),
+                "stamp")
+
+    def stamps_view(self, rank):
+        return self.buffer(rank, N.MX_BUF_STAMPS, torch.int64, (64,))
+
     def dispatch(self, x, rank=None, stream=None):
         N.check(N.load().mx_dispatch(self._plan, self._r(rank),
                                      C.c_void_p(x.data_ptr()), stream_ptr(stream)),

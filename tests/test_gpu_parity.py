@@ -366,6 +366,35 @@ def test_layer_graph_replay_matches_eager_and_oracle():
     layer.close()
 
 
+def test_measured_phases_and_stamped_trace():
+    """Device-clock stamps bracket every phase in order; the stamped trace
+    carries the reference's events with spans inside the measured run."""
+    from paper_2601_08800_b200 import SwiGLUExperts
+    from paper_2601_08800_b200.layer import MoELayer
+    from paper_2601_08800_b200.measured import layer_trace, measure_phases, stamp_trace
+    T, h, E, k, I = 512, 256, 32, 4, 256
+    ex = SwiGLUExperts.random(E, h, I, seed=9)
+    for wire in ("slot", "token"):
+        layer = MoELayer(1, 1, T, h, E, k, I, experts=ex, rank=0, wire=wire)
+        gen = torch.Generator(device="cuda").manual_seed(2)
+        x = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
+        logits = torch.randn(T, E, device="cuda", generator=gen)
+        layer.forward(x, logits)
+        ph = measure_phases(layer, x, logits, iters=3)
+        names = layer.phase_names()[1:]
+        assert list(ph) == names
+        prev = 0.0
+        for nm in names:
+            a, b = ph[nm]
+            assert prev <= a + 1e-12 and a <= b
+            prev = b
+        assert ph["gemm1_swiglu"][1] - ph["gemm1_swiglu"][0] > 0
+        events, stages = layer_trace(layer)
+        text = stamp_trace(events, stages, [ph], wire)
+        assert text.count("expert_compute") == sum(1 for e in events if e.op == "expert_compute")
+        layer.close()
+
+
 # ----------------------------------------------------------------- wire TOKEN
 @pytest.mark.parametrize("shape", [(1, 1), (2, 1), (2, 2), (4, 2), (2, 4), (8, 1), (4, 4)])
 def test_wire_token_f64_affine_emulated(shape):
