@@ -74,10 +74,11 @@ def main():
     xs = [x[i * Tm:(i + 1) * Tm] for i in range(mb)]
     ls = [lg[i * Tm:(i + 1) * Tm] for i in range(mb)]
     y = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
-    main_s = torch.cuda.current_stream()
-    streams = [main_s] + [torch.cuda.Stream() for _ in range(mb - 1)]
+    side = [torch.cuda.Stream() for _ in range(mb - 1)]
 
     def step():
+        main_s = torch.cuda.current_stream()   # the capture stream inside the graph
+        streams = [main_s] + side
         start = torch.cuda.Event()
         start.record(main_s)
         gate = start
@@ -93,7 +94,7 @@ def main():
                 expert(L, s)
                 post(L, s)
                 y[i * Tm:(i + 1) * Tm].copy_(L.y, non_blocking=True)
-        for s in streams[1:]:
+        for s in side:
             main_s.wait_stream(s)
 
     for _ in range(2):
@@ -108,6 +109,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(5):
         graph.replay()
+    main_s = torch.cuda.current_stream()
     ev = []
     for _ in range(args.iters):
         flush.fill_(1)
