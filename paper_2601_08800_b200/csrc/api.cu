@@ -225,17 +225,18 @@ static DevView view_for(const mx_plan* p, int r) {
   return v;
 }
 
-// GEMM1 gathers token rows (TMA tile::gather4) instead of reading a
-// materialised expert-major copy: SwiGLU experts, and either one group
-// (rows straight from x) or the TOKEN wire (rows from the XBUF).
-// Measured on B200 (round 1): 32 gather4 ops per k-block throttle the TMA
-// producer -- GEMM1 964 us vs 374 us with the copy -- so it is opt-in
-// (MX_GATHER=1) until the producer is rebuilt on LDGSTS.
+// GEMM1 gathers its A rows through a row table (16 B LDGSTS in the GEMM
+// producer) instead of reading a materialised expert-major copy: SwiGLU
+// experts, and either one group (rows straight from x, no dispatch copy) or
+// the TOKEN wire (rows from the XBUF, no expand).  Opt-in (MX_GATHER=1,
+// read per call): measured on B200 at config B N=1, GEMM1 takes 613 us with
+// the gathering producer vs 354 us on the TMA-tiled copy, which outweighs
+// the 60 us dispatch copy it removes (the old TMA tile::gather4 producer:
+// 964 us).  Two stages of 128 scattered rows in flight per CTA cannot hide
+// L2 latency; the tiled TMA path keeps four 48 KB stages in flight.
 static bool gathers(const mx_plan* p) {
-  static const bool enabled = [] {
-    const char* e = getenv("MX_GATHER");
-    return e && e[0] == '1';
-  }();
+  const char* e = getenv("MX_GATHER");
+  const bool enabled = e && e[0] == '1';
   return enabled && p->d.expert_kind == MX_EXPERT_SWIGLU &&
          (p->d.wire == MX_WIRE_TOKEN || p->d.n_group == 1);
 }

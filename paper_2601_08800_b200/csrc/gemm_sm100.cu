@@ -32,6 +32,8 @@ constexpr int BK = 64;   // bf16 elements per k-block: 128 B rows, one SWIZZLE_1
 constexpr int BKB = 128; // bytes per k-block row (64 bf16 or 128 e4m3)
 constexpr int NUM_THREADS = 256;      // CTA-pair kernel: 4 epilogue warps
 constexpr int NUM_THREADS_1 = 384;    // single-CTA kernel: warps 4..11 = 8 epilogue warps
+constexpr int GATHER_THREADS = 64;    // gathered A: warps 0 and 3 issue the row LDGSTS
+constexpr int GATHER_LAG = 2;         // stages a gathering thread runs ahead of its arrive
 
 template <int BN>
 struct Cfg {
@@ -76,15 +78,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 }
 // 4 rows (row coordinates r0..r3, negative = zero fill) x 64 columns into
 // 512 contiguous bytes of smem, 128B swizzle applied by the TMA unit.
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int col, int4 rows) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(rows.x),
-      "r"(rows.y), "r"(rows.z), "r"(rows.w)
-      : "memory");
+// 16-byte LDGSTS (L2 only); src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -295,7 +301,8 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      // GATHER: the B TMA arrive + one arrive per gathering thread
+      mbar_init(&full[s], GATHER ? 1 + GATHER_THREADS : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -316,36 +323,65 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   const uint32_t tmem = s_tmem;
   const int total_tiles = s_tstart[G];
 
-  if (warp == 0) {
+  if (warp == 0 || (GATHER && warp == 3)) {
     if constexpr (GATHER) {
-      // ===== TMA producer, gathered A: lane l brings rows 4l..4l+3 of the
-      // 128-row A tile with one tile::gather4 per k-block; lane 0 owns the
-      // barrier protocol and the B tile.
+      // ===== gathering producer (warps 0 and 3): A rows come from an
+      // arbitrary row table (token rows of x / XBUF), so they are brought
+      // with 16 B LDGSTS into the 128B-swizzled layout the UMMA descriptor
+      // expects (row r at r*128, chunk c at (c ^ (r & 7)) * 16); B by TMA.
+      // Thread pt owns rows pt and pt + 64.  LDGSTS writes are generic-proxy:
+      // each thread waits for its group GATHER_LAG stages later, fences to
+      // the async proxy and only then arrives on the stage's full barrier.
+      const int pt = (warp == 0 ? 0 : 32) + lane;
+      const char* abase = args.a_base;
+      const long long lda = args.lda;
       int stage = 0;
       uint32_t phase = 0;
+      int issued = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int g, mb, nb;
         decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
         const int bg = args.b_index ? args.b_index[g] : g;
         const int b_row = bg * args.N + nb * BN;
-        const int r_local = mb * BM + 4 * lane;
-        const long long base = (long long)s_off[g] + r_local;
-        int4 rows;
-        rows.x = r_local + 0 < s_cnt[g] ? args.a_rows[base + 0] : -1;
-        rows.y = r_local + 1 < s_cnt[g] ? args.a_rows[base + 1] : -1;
-        rows.z = r_local + 2 < s_cnt[g] ? args.a_rows[base + 2] : -1;
-        rows.w = r_local + 3 < s_cnt[g] ? args.a_rows[base + 3] : -1;
+        const int cnt = s_cnt[g];
+        const char* src[2];
+        int sz[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r_local = mb * BM + pt + 64 * h;
+          const int row = r_local < cnt ? args.a_rows[(long long)s_off[g] + r_local] : -1;
+          src[h] = row >= 0 ? abase + (long long)row * lda : abase;
+          sz[h] = row >= 0 ? 16 : 0;
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
-          if (lane == 0) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (pt == 0) {
+            mbar_expect_tx(&full[stage], C::B_BYTES);
             tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
           }
-          __syncwarp();
-          tma_gather4(sA + stage * C::A_BYTES + lane * 512, &map_a, &full[stage], kb * KE, rows);
+          const uint32_t dst = smem_u32(sA + stage * C::A_BYTES);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = pt + 64 * h;
+            const char* sp = src[h] + kb * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              cp_async16(dst + r * 128 + ((c ^ (r & 7)) << 4), sp + c * 16, sz[h]);
+          }
+          cp_async_commit();
+          if (issued >= GATHER_LAG) {
+            cp_async_wait<GATHER_LAG>();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&full[(stage + C::STAGES - GATHER_LAG) % C::STAGES]);
+          }
+          ++issued;
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      cp_async_wait<0>();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int j = (issued < GATHER_LAG ? issued : GATHER_LAG); j >= 1; --j)
+        mbar_arrive(&full[(stage + C::STAGES - j) % C::STAGES]);
     } else if (lane == 0) {
       // ===== TMA producer
       int stage = 0;
@@ -901,19 +937,21 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   CUtensorMap ma, mb, md;
   memset(&md, 0, sizeof(md));
   const bool gather = a_rows != nullptr;
-  // gathered A: box of 64 columns x 1 row, addressed 4 rows at a time
-  int rc = gather ? make_map(&ma, A, a_src_rows, K, 1) : make_map(&ma, A, M_cap, K, BM);
-  if (rc) return rc;
+  (void)a_src_rows;
   // B rows: every group's N rows (b_index may address any of them)
   long long b_rows = (long long)G * N;
-  rc = make_map(&mb, B, b_rows, K, bn);
+  int rc = make_map(&mb, B, b_rows, K, bn);
   if (rc) return rc;
+  // gathered A is read with LDGSTS through a_rows (no tensor map)
+  if (gather) ma = mb;
+  else if ((rc = make_map(&ma, A, M_cap, K, BM))) return rc;
   if (out_dtype == MX_BF16) {  // 32x32 output boxes, 64 B swizzle (staged epilogue)
     rc = make_map(&md, D, M_cap, swiglu ? N / 2 : N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
   Args a{};
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
+  if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
   a.M_cap = M_cap;
   // upper bound on tiles (host does not know the per-group counts)

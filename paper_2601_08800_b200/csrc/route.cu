@@ -18,11 +18,19 @@
 
 namespace mx {
 
+// Warp-wide fp32 max in one instruction (CREDUX.MAX.F32, sm_100a).
+__device__ __forceinline__ float warp_max_f32(float v) {
+  float m;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(v));
+  return m;
+}
+
 // Fused softmax + top-k gate: one warp per token over all SMs.  Lane owns
 // experts e = 128*i + 4*lane + q (128-bit coalesced row loads).  Selection
 // key: fp32 logit descending, lowest id on ties (exact compares, so ids are
 // bit-exact with the oracle).  Each lane caches its best untaken candidate;
-// only the winning lane rescans, so a round is one 5-level warp argmax.
+// only the winning lane rescans.  A round is two warp reductions: the max
+// key (redux.sync.max.f32) and the lowest id holding it (redux.sync.min).
 template <class WT, int EV>
 __global__ void __launch_bounds__(256)
 k_gate(DevView v, const float* __restrict__ logits) {
@@ -65,14 +73,8 @@ k_gate(DevView v, const float* __restrict__ logits) {
   int my_e = 0;
   float my_v = 0.f;
   for (int r = 0; r < k; ++r) {
-    float bv = cv;
-    int be = ce;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-      if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
-    }
+    const float bv = warp_max_f32(cv);
+    const int be = (int)__reduce_min_sync(0xffffffffu, cv == bv ? (unsigned)ce : 0xffffffffu);
     if (lane == r) { my_e = be; my_v = bv; }
     if (be == ce) {  // this lane owned the winner
       taken |= 1u << (4 * (be >> 7) + (be & 3));
@@ -193,14 +195,8 @@ k_gate_grouped(DevView v, const float* __restrict__ logits) {
   int my_e = 0;
   float my_s = 0.f;
   for (int r = 0; r < k; ++r) {
-    float bv = cv;
-    int be = ce;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-      if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
-    }
+    const float bv = warp_max_f32(cv);
+    const int be = (int)__reduce_min_sync(0xffffffffu, cv == bv ? (unsigned)ce : 0xffffffffu);
     const unsigned own = __ballot_sync(0xffffffffu, be == ce);
     const float ws = __shfl_sync(0xffffffffu, cs, __ffs(own) - 1);
     if (lane == r) { my_e = be; my_s = ws; }

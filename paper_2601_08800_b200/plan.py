@@ -23,7 +23,7 @@ from .errors import StrategyError
 
 DTYPES = {torch.float64: N.MX_F64, torch.float32: N.MX_F32,
           torch.bfloat16: N.MX_BF16}
-_TYPESTR = {torch.float64: "<f8", torch.float32: "<f4", torch.int32: "<i4",
+_TYPESTR = {torch.float64: "<f8", torch.float32: "<f4", torch.int32: "<i4", torch.int64: "<i8",
             torch.bfloat16: "<i2"}
 
 

@@ -366,6 +366,32 @@ def test_layer_graph_replay_matches_eager_and_oracle():
     layer.close()
 
 
+@pytest.mark.parametrize("wire", ["slot", "token"])
+def test_gathered_gemm1_equals_copied_rows(wire, monkeypatch):
+    """GEMM1 gathering A rows through the row table (LDGSTS producer) gives
+    the same bits as the materialised expert-major copy (MX_GATHER=0, the
+    default)."""
+    from paper_2601_08800_b200 import SwiGLUExperts
+    from paper_2601_08800_b200.layer import MoELayer
+    T, h, E, k, I = 1000, 512, 16, 4, 256
+    ex = SwiGLUExperts.random(E, h, I, seed=4)
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = torch.randn(T, E, device="cuda", generator=gen)
+    outs = {}
+    for g in ("0", "1"):
+        monkeypatch.setenv("MX_GATHER", g)
+        layer = MoELayer(1, 1, T, h, E, k, I, experts=ex, rank=0, wire=wire)
+        outs[g] = layer.forward(x, logits).clone()
+        layer.close()
+    assert torch.equal(outs["0"], outs["1"])
+    oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
+    assert orc.verify_metric(outs["1"].float().cpu().numpy(), y_o) <= 2e-2
+
+
 def test_measured_phases_and_stamped_trace():
     """Device-clock stamps bracket every phase in order; the stamped trace
     carries the reference's events with spans inside the measured run."""
