@@ -66,6 +66,27 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
       if (u < 0) continue;
       if (d == v.group) {
         copy_row(at<char>(v, v.rank, v.off.xbuf) + (size_t)u * row_bytes, row, row_bytes, lane);
+      } else if (((sh_off | sh_bytes | row_bytes) & 15) == 0) {
+        // the shard is loaded once and stored to every TP rank of host d
+        // (4 x 16 B per lane in flight per pass)
+        const char* src = row + sh_off;
+        const size_t nv = sh_bytes >> 4;
+        for (size_t i = lane; i < nv; i += 128) {
+          uint4 val[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (i + 32 * q < nv) val[q] = ld_v4(src + ((i + 32 * q) << 4));
+          for (int tt = 0; tt < m; ++tt) {
+            char* dst = at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes + sh_off;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (i + 32 * q < nv) st_v4(dst + ((i + 32 * q) << 4), val[q]);
+          }
+        }
+        if (tail)
+          for (int tt = 0; tt < m; ++tt)
+            copy_row(at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes + body,
+                     row + body, row_bytes - body, lane);
       } else {
         for (int tt = 0; tt < m; ++tt) {
           char* dst = at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes;
@@ -239,7 +260,65 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
       const int u = upos[t * n + d];
       if (u >= 0 && nh < HMAX) { hs[nh] = d; us[nh] = u; ++nh; }
     }
-    for (int c = c0 + lane * V; c < c1; c += 32 * V) {
+    int c = c0 + lane * V;
+    if (m * nh <= 4) {
+      // fast path: every (TP rank, host) z load of two column vectors is
+      // issued before any is consumed (<= 8 remote 16 B loads in flight per
+      // lane); the sum keeps the TP-rank-major, arrival-order association
+      const T* src[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int tt = i / (nh > 0 ? nh : 1), a = i % (nh > 0 ? nh : 1);
+        src[i] = i < m * nh ? at<T>(v, hs[a] * m + tt, v.off.z) + (size_t)us[a] * h : nullptr;
+      }
+      for (; c + 32 * V < c1; c += 64 * V) {
+        uint4 r0[4], r1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < m * nh) {
+            r0[i] = ld_v4(src[i] + c);
+            r1[i] = ld_v4(src[i] + c + 32 * V);
+          }
+        A a0[V], a1[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) a0[q] = a1[q] = (A)0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < m * nh) {
+            const T* p0 = reinterpret_cast<const T*>(&r0[i]);
+            const T* p1 = reinterpret_cast<const T*>(&r1[i]);
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              a0[q] = add_rn(a0[q], to_acc(p0[q]));
+              a1[q] = add_rn(a1[q], to_acc(p1[q]));
+            }
+          }
+        if (v.Is_t)
+          for (int tt = 0; tt < m; ++tt) {
+            const T* ps = at<T>(v, j * m + tt, v.off.part_s) + (size_t)t * h + c;
+            const uint4 s0 = ld_v4(ps), s1 = ld_v4(ps + 32 * V);
+            const T* q0 = reinterpret_cast<const T*>(&s0);
+            const T* q1 = reinterpret_cast<const T*>(&s1);
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              a0[q] = add_rn(a0[q], to_acc(q0[q]));
+              a1[q] = add_rn(a1[q], to_acc(q1[q]));
+            }
+          }
+        T o0[V], o1[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          o0[q] = from_acc<T>(a0[q]);
+          o1[q] = from_acc<T>(a1[q]);
+        }
+        for (int tt = 0; tt < m; ++tt) {
+          T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)t * h + c;
+          st_v4(y, *reinterpret_cast<uint4*>(o0));
+          st_v4(y + 32 * V, *reinterpret_cast<uint4*>(o1));
+        }
+      }
+    }
+    for (; c < c1; c += 32 * V) {
       A acc[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) acc[q] = (A)0;
