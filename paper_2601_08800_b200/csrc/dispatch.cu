@@ -81,12 +81,84 @@ __global__ void __launch_bounds__(256) k_dispatch(DevView v, const char* __restr
   }
 }
 
+// Token-major form for rows of at most VPL x 512 B: warp per token, the row
+// is loaded into registers once (VPL x 16 B per lane) and stored to every
+// one of the token's k slot rows (full row locally, column shard to each TP
+// rank of a remote host).  Same destinations and bytes as k_dispatch.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_dispatch_rows(DevView v, const char* __restrict__ x) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int* ids = at<int>(v, v.rank, v.off.ids);
+  const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
+  const size_t row_bytes = (size_t)v.wrow;
+  const int nvec = (int)(row_bytes >> 4);
+  const size_t body = (size_t)v.h * v.welt;
+  int c0, c1;
+  col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
+  const int v0 = (int)(((size_t)c0 * v.welt) >> 4), v1 = (int)(((size_t)c1 * v.welt) >> 4);
+  const int vt = (int)(body >> 4);  // first vector of the scale tail
+  const bool tail = v.tp_rank == 0 && row_bytes > body;
+  for (long long t = gw; t < v.T; t += nwarps) {
+    int e = 0, pos = 0;
+    if (lane < v.k) {
+      e = ids[t * v.k + lane];
+      pos = slot_pos[t * v.k + lane];
+    }
+    uint4 val[VPL];
+    const char* row = x + (size_t)t * row_bytes;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q)
+      if (q * 32 + lane < nvec) val[q] = ld_nc_v4(row + ((size_t)(q * 32 + lane) << 4));
+    for (int sl = 0; sl < v.k; ++sl) {
+      const int es = __shfl_sync(0xffffffffu, e, sl);
+      const long long p = __shfl_sync(0xffffffffu, pos, sl);
+      if (p >= v.cap) continue;  // flagged by the layout; never write out of bounds
+      const int d = home_of(es, v.n, v.E);
+      if (d == v.group) {
+        char* dst = at<char>(v, v.rank, v.off.recv) + p * row_bytes;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q)
+          if (q * 32 + lane < nvec) st_v4(dst + ((size_t)(q * 32 + lane) << 4), val[q]);
+      } else {
+        for (int tt = 0; tt < v.m; ++tt) {
+          char* dst = at<char>(v, d * v.m + tt, v.off.recv) + p * row_bytes;
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int vi = q * 32 + lane;
+            if ((vi >= v0 && vi < v1) || (tail && vi >= vt && vi < nvec))
+              st_v4(dst + ((size_t)vi << 4), val[q]);
+          }
+        }
+      }
+    }
+  }
+}
+
 int launch_dispatch(const DevView& v, const void* x, cudaStream_t s) {
   const long long total = (long long)v.T * v.k;
   if (total == 0) return MX_OK;
+  const char* xp = static_cast<const char*>(x);
+  const size_t row_bytes = (size_t)v.wrow;
+  int c0, c1;
+  col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
+  const bool aligned = (row_bytes % 16) == 0 && ((size_t)c0 * v.welt) % 16 == 0 &&
+                       ((size_t)c1 * v.welt) % 16 == 0 && ((size_t)v.h * v.welt) % 16 == 0 &&
+                       v.k <= 32;
+  if (aligned && row_bytes <= 8 * 512) {
+    long long blocks = (v.T + 7) / 8;  // warp per token
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (row_bytes <= 2 * 512) pdl_launch(k_dispatch_rows<2>, (int)blocks, 256, 0, s, v, xp);
+    else if (row_bytes <= 4 * 512) pdl_launch(k_dispatch_rows<4>, (int)blocks, 256, 0, s, v, xp);
+    else pdl_launch(k_dispatch_rows<8>, (int)blocks, 256, 0, s, v, xp);
+    MX_LAUNCH_CHECK();
+    return MX_OK;
+  }
   long long blocks = (total + 7) / 8;  // 8 warps per CTA, one slot per warp
   if (blocks > 148 * 16) blocks = 148 * 16;
-  pdl_launch(k_dispatch, (int)blocks, 256, 0, s, v, static_cast<const char*>(x));
+  pdl_launch(k_dispatch, (int)blocks, 256, 0, s, v, xp);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
