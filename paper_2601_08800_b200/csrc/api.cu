@@ -536,9 +536,12 @@ int mx_dispatch(mx_plan* p, int rank, const void* x, void* stream) {
       xg = xq;
     }
     if (p->d.wire == MX_WIRE_TOKEN) {
-      rc = launch_dispatch_token(v, xg, s);
+      // decided before the launch: without the gathered GEMM1 the dispatch
+      // writes own-group rows straight into RECV (and expand skips them)
       p->a_src[r] = gathers(p) ? static_cast<const void*>(p->comm->heap[r] + p->off.xbuf) : nullptr;
       p->a_src_rows[r] = (long long)p->d.tokens * p->d.n_group;
+      v.a_src = p->a_src[r];
+      rc = launch_dispatch_token(v, xg, s);
     } else if (gathers(p)) {
       rc = launch_rowsrc_slot(v, s);  // n == 1: no row copies at all
       p->a_src[r] = xg;

@@ -68,8 +68,13 @@ __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
       // which halves the live registers.
       constexpr bool EXACT = DT == MX_F64;
       A ws[KU];
+      const T* bp[KU];  // slot rows on the host's TP rank 0 (tt = 0)
 #pragma unroll
-      for (int s = 0; s < KU; ++s) ws[s] = s_w[warp][s < k ? s : 0];
+      for (int s = 0; s < KU; ++s) {
+        const int ss = s < k ? s : 0;
+        ws[s] = s_w[warp][ss];
+        bp[s] = at<T>(v, s_src[warp][ss], v.off.partial) + (size_t)s_pos[warp][ss] * h;
+      }
       for (int c = c0 + lane * V; c < c1; c += 32 * V) {
         A red[EXACT ? KU : 1][V];
         A acc[V];
@@ -82,8 +87,9 @@ __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
 #pragma unroll
           for (int s = 0; s < KU; ++s) {
             if (s < k) {
-              const int r = s_src[warp][s] + tt;
-              const T* p = at<T>(v, r, v.off.partial) + (size_t)s_pos[warp][s] * h + c;
+              const T* p = tt == 0 ? bp[s] + c
+                                   : at<T>(v, s_src[warp][s] + tt, v.off.partial) +
+                                         (size_t)s_pos[warp][s] * h + c;
               if constexpr (VEC) raw[s] = ld_v4(p);
               else { T one = *p; raw[s].x = 0; *reinterpret_cast<T*>(&raw[s]) = one; }
             }

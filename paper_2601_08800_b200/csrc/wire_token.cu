@@ -59,12 +59,39 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
   col_shard(v.h, m, v.tp_rank, &c0, &c1);
   const size_t sh_off = (size_t)c0 * v.welt, sh_bytes = (size_t)(c1 - c0) * v.welt;
   const bool tail = v.tp_rank == 0 && row_bytes > body;
+  // own-group rows go straight to their expert-major RECV rows (the local
+  // hop needs no dedup); the XBUF keeps them only for the gathered GEMM1
+  const bool direct_local = v.a_src == nullptr && (row_bytes & 15) == 0;
   for (long long t = gw; t < v.T; t += nwarps) {
     const char* row = x + (size_t)t * row_bytes;
     for (int d = 0; d < n; ++d) {
       const int u = upos[t * n + d];
       if (u < 0) continue;
-      if (d == v.group) {
+      if (d == v.group && direct_local) {
+        // rows of this token's slots on the own host (pos < cap: layout-checked)
+        int pos = -1;
+        if (lane < k) {
+          const int e = ids[t * k + lane];
+          const int p = slot_pos[t * k + lane];
+          if (home_of(e, n, E) == d && p < v.cap) pos = p;
+        }
+        const unsigned mine = __ballot_sync(0xffffffffu, pos >= 0);
+        char* recv = at<char>(v, v.rank, v.off.recv);
+        const size_t nv = row_bytes >> 4;
+        for (size_t i = lane; i < nv; i += 128) {
+          uint4 val[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (i + 32 * q < nv) val[q] = ld_v4(row + ((i + 32 * q) << 4));
+          for (unsigned b = mine; b; b &= b - 1) {
+            const int p = __shfl_sync(0xffffffffu, pos, __ffs(b) - 1);
+            char* dst = recv + (size_t)p * row_bytes;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (i + 32 * q < nv) st_v4(dst + ((i + 32 * q) << 4), val[q]);
+          }
+        }
+      } else if (d == v.group) {
         copy_row(at<char>(v, v.rank, v.off.xbuf) + (size_t)u * row_bytes, row, row_bytes, lane);
       } else if (((sh_off | sh_bytes | row_bytes) & 15) == 0) {
         // the shard is loaded once and stored to every TP rank of host d
@@ -138,7 +165,15 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
   const size_t row_bytes = (size_t)v.wrow;
   const char* xbuf = at<char>(v, v.rank, v.off.xbuf);
   char* recv = at<char>(v, v.rank, v.off.recv);
+  // own-group pairs were written straight into RECV by the dispatch
+  long long skip0 = 0, skip1 = 0;
+  if (v.a_src == nullptr && (row_bytes & 15) == 0) {
+    const int g = v.group;
+    skip0 = at<int>(v, v.rank, v.off.poff)[g * v.n + g];
+    skip1 = skip0 + at<int>(v, v.rank, v.off.ucnt_all)[g * v.n + g];
+  }
   for (long long u = gw; u < pairs; u += nwarps) {
+    if (u >= skip0 && u < skip1) continue;
     const int cnt = pn[u];
     int rows[MX_KMAX];
     for (int i = 0; i < cnt; ++i) rows[i] = pe[u * v.KH + i].p;
