@@ -33,7 +33,9 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 // scope), then wait until every peer has published it into ours (acquire).
 // One thread per peer.  A watchdog turns a lost peer into an error flag
 // instead of a hang (SURVEY.md §5 failure detection).
-__global__ void k_barrier(DevView v) {
+// Ranks [r0, r0 + nr) take part (the whole world, or one TP group); every
+// rank still advances its epoch, so full and group barriers interleave.
+__global__ void k_barrier(DevView v, int r0, int nr) {
   pdl_wait();  // predecessor's outputs are visible after this
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) {
@@ -45,8 +47,8 @@ __global__ void k_barrier(DevView v) {
   }
   __syncthreads();
   const unsigned long long epoch = s_epoch;
-  const int r = threadIdx.x;
-  if (r < v.W) {
+  const int r = r0 + threadIdx.x;
+  if ((int)threadIdx.x < nr) {
     __threadfence_system();
     st_release_sys(at<unsigned long long>(v, r, v.off.flags) + v.rank, epoch);
     const unsigned long long* mine = at<unsigned long long>(v, v.rank, v.off.flags) + r;
@@ -62,8 +64,9 @@ __global__ void k_barrier(DevView v) {
   __threadfence_system();
 }
 
-int launch_barrier(const DevView& v, cudaStream_t s) {
-  pdl_launch(k_barrier, 1, 64, 0, s, v);
+int launch_barrier(const DevView& v, cudaStream_t s, bool group_only) {
+  const int r0 = group_only ? v.group * v.m : 0, nr = group_only ? v.m : v.W;
+  pdl_launch(k_barrier, 1, 64, 0, s, v, r0, nr);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -452,11 +455,11 @@ const char* group_ptr(const mx_plan* p, const void* base, int group, size_t per_
   return static_cast<const char*>(base) + (size_t)group * p->d.tokens * per_token_bytes;
 }
 
-int barrier(mx_plan* p, cudaStream_t s) {
+int barrier(mx_plan* p, cudaStream_t s, bool group_only = false) {
   mx_comm* c = p->comm;
   if (c->emulate || c->W == 1) return MX_OK;
   DevView v = view_for(p, c->rank);
-  return launch_barrier(v, s);
+  return launch_barrier(v, s, group_only);
 }
 
 int check_errors(mx_plan* p, int first, int last) {
@@ -646,7 +649,10 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
   if ((rc = mx_expert(p, rank, ep, stream))) return rc;
   if ((rc = barrier(p, s))) return rc;            // every partial written
   if ((rc = mx_combine(p, rank, nullptr, stream))) return rc;
-  if ((rc = barrier(p, s))) return rc;            // y complete; buffers reusable
+  // y complete: every TP peer of the group pushed its shard.  Group-local --
+  // nothing of another group is touched before the next forward's first
+  // full barrier (its route only writes count rows read after that barrier)
+  if ((rc = barrier(p, s, true))) return rc;
   if (y_out) {
     RankIter it;
     if ((rc = ranks_for(p, rank, &it))) return rc;
