@@ -933,7 +933,12 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   if (swiglu && (N % 256 != 0 || out_dtype != MX_BF16)) { set_error("grouped_gemm: SwiGLU needs N %% 256 == 0 and bf16 out"); return MX_ERR_UNSUPPORTED; }
   if (out_dtype != MX_BF16 && out_dtype != MX_F32) { set_error("grouped_gemm: out dtype"); return MX_ERR_UNSUPPORTED; }
   if (M_cap < 1) return MX_OK;
-  const int bn = (N % 256 == 0) ? 256 : 128;
+  // BN = 256 unless N forbids it -- or the GEMM is weight-streaming (decode:
+  // at most 64 rows per group on average), where the finer 128-column tiles
+  // spread the weight reads over more CTAs (SwiGLU needs the 256 tile: its
+  // gate/up halves are interleaved in 128-row blocks of w13)
+  const bool small_m = M_cap <= 64LL * G;
+  const int bn = (N % 256 == 0 && (swiglu || !small_m)) ? 256 : 128;
   CUtensorMap ma, mb, md;
   memset(&md, 0, sizeof(md));
   const bool gather = a_rows != nullptr;
