@@ -17,6 +17,8 @@
 
 namespace mx {
 
+constexpr int DSPLIT = 2;  // warps per token in the dispatch
+
 // One pair-list entry: expert-major row of the slot and its top-k weight,
 // written with a single remote store.
 template <class WT> struct PairEnt;
@@ -46,8 +48,11 @@ template <class WT>
 __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* __restrict__ x) {
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
+  // DSPLIT warps per token, each moving its slice of the row's 16 B vectors
+  // (more stores in flight per SM); warp 0 of a token also writes metadata
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int sub = (int)(gw % DSPLIT);
   const int n = v.n, m = v.m, k = v.k, E = v.E;
   const int* ids = at<int>(v, v.rank, v.off.ids);
   const WT* wts = at<WT>(v, v.rank, v.off.w);
@@ -61,8 +66,12 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
   const bool tail = v.tp_rank == 0 && row_bytes > body;
   // own-group rows go straight to their expert-major RECV rows (the local
   // hop needs no dedup); the XBUF keeps them only for the gathered GEMM1
-  const bool direct_local = v.a_src == nullptr && (row_bytes & 15) == 0;
-  for (long long t = gw; t < v.T; t += nwarps) {
+  const bool aligned = ((sh_off | sh_bytes | row_bytes) & 15) == 0;
+  const bool direct_local = v.a_src == nullptr && aligned;
+  const size_t nv_row = row_bytes >> 4, nv_sh = sh_bytes >> 4;
+  const size_t r_lo = sub * nv_row / DSPLIT, r_hi = (sub + 1) * nv_row / DSPLIT;
+  const size_t s_lo = sub * nv_sh / DSPLIT, s_hi = (sub + 1) * nv_sh / DSPLIT;
+  for (long long t = gw / DSPLIT; t < v.T; t += nwarps / DSPLIT) {
     const char* row = x + (size_t)t * row_bytes;
     for (int d = 0; d < n; ++d) {
       const int u = upos[t * n + d];
@@ -77,44 +86,42 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
         }
         const unsigned mine = __ballot_sync(0xffffffffu, pos >= 0);
         char* recv = at<char>(v, v.rank, v.off.recv);
-        const size_t nv = row_bytes >> 4;
-        for (size_t i = lane; i < nv; i += 128) {
+        for (size_t i = r_lo + lane; i < r_hi; i += 128) {
           uint4 val[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (i + 32 * q < nv) val[q] = ld_v4(row + ((i + 32 * q) << 4));
+            if (i + 32 * q < r_hi) val[q] = ld_v4(row + ((i + 32 * q) << 4));
           for (unsigned b = mine; b; b &= b - 1) {
             const int p = __shfl_sync(0xffffffffu, pos, __ffs(b) - 1);
             char* dst = recv + (size_t)p * row_bytes;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              if (i + 32 * q < nv) st_v4(dst + ((i + 32 * q) << 4), val[q]);
+              if (i + 32 * q < r_hi) st_v4(dst + ((i + 32 * q) << 4), val[q]);
           }
         }
       } else if (d == v.group) {
-        copy_row(at<char>(v, v.rank, v.off.xbuf) + (size_t)u * row_bytes, row, row_bytes, lane);
-      } else if (((sh_off | sh_bytes | row_bytes) & 15) == 0) {
+        if (sub == 0)
+          copy_row(at<char>(v, v.rank, v.off.xbuf) + (size_t)u * row_bytes, row, row_bytes, lane);
+      } else if (aligned) {
         // the shard is loaded once and stored to every TP rank of host d
-        // (4 x 16 B per lane in flight per pass)
         const char* src = row + sh_off;
-        const size_t nv = sh_bytes >> 4;
-        for (size_t i = lane; i < nv; i += 128) {
+        for (size_t i = s_lo + lane; i < s_hi; i += 128) {
           uint4 val[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (i + 32 * q < nv) val[q] = ld_v4(src + ((i + 32 * q) << 4));
+            if (i + 32 * q < s_hi) val[q] = ld_v4(src + ((i + 32 * q) << 4));
           for (int tt = 0; tt < m; ++tt) {
             char* dst = at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes + sh_off;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              if (i + 32 * q < nv) st_v4(dst + ((i + 32 * q) << 4), val[q]);
+              if (i + 32 * q < s_hi) st_v4(dst + ((i + 32 * q) << 4), val[q]);
           }
         }
-        if (tail)
+        if (tail && sub == 0)
           for (int tt = 0; tt < m; ++tt)
             copy_row(at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes + body,
                      row + body, row_bytes - body, lane);
-      } else {
+      } else if (sub == 0) {
         for (int tt = 0; tt < m; ++tt) {
           char* dst = at<char>(v, d * m + tt, v.off.xbuf) + (size_t)u * row_bytes;
           copy_row(dst + sh_off, row + sh_off, sh_bytes, lane);
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
         }
       }
     }
+    if (sub != 0) continue;
     // metadata: lane i carries slot i
     int e = 0, d = -1;
     if (lane < k) {
@@ -426,8 +434,9 @@ int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s) {
   int rc = check_vec(v);
   if (rc) return rc;
   if (v.T == 0) return MX_OK;
-  if (v.elt == 8) pdl_launch(k_dispatch_token<double>, blocks_for(v.T), 256, 0, s, v, static_cast<const char*>(x));
-  else pdl_launch(k_dispatch_token<float>, blocks_for(v.T), 256, 0, s, v, static_cast<const char*>(x));
+  const int g = blocks_for((long long)v.T * DSPLIT);
+  if (v.elt == 8) pdl_launch(k_dispatch_token<double>, g, 256, 0, s, v, static_cast<const char*>(x));
+  else pdl_launch(k_dispatch_token<float>, g, 256, 0, s, v, static_cast<const char*>(x));
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
