@@ -219,38 +219,6 @@ k_gate_grouped(DevView v, const float* __restrict__ logits) {
   }
 }
 
-// Exclusive prefix of the chunk counts for row w (experts, then hosts, then
-// pairs) by one warp, coalesced over the expert-major [E][C] layout;
-// publishes the group's per-expert totals into every rank's count matrix
-// (peer stores in SPMD) and the (token, host) pair totals likewise.  Rows
-// written by other CTAs of this launch are read through L2 (ld.cg).
-__device__ __forceinline__ void scan_row(const DevView& v, int w, int lane) {
-  const int E = v.E, n = v.n, C = v.C;
-  int* row;
-  if (w < E) row = at<int>(v, v.rank, v.off.chunk_hist) + (size_t)w * C;
-  else if (w < E + n) row = at<int>(v, v.rank, v.off.chunk_host) + (size_t)(w - E) * C;
-  else row = at<int>(v, v.rank, v.off.chunk_pair) + (size_t)(w - E - n) * C;
-  int carry = 0;
-  for (int base = 0; base < C; base += 32) {
-    const int c = base + lane;
-    const int x = (c < C) ? __ldcg(row + c) : 0;
-    int incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (c < C) row[c] = carry + incl - x;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  if (w < E) {
-    for (int r = lane; r < v.W; r += 32) at<int>(v, r, v.off.cnt_all)[v.group * E + w] = carry;
-  } else if (w >= E + n) {
-    const int d = w - E - n;
-    for (int r = lane; r < v.W; r += 32) at<int>(v, r, v.off.ucnt_all)[v.group * n + d] = carry;
-  }
-}
-
 // One CTA per chunk of MX_CHUNK tokens of this rank's group.
 template <class WT>
 __global__ void __launch_bounds__(512)
@@ -375,20 +343,46 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     chunk_hist[e * v.C + c] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
                               __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
   }
-  // the last CTA to finish runs the chunk scans (no separate launch)
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int* ctr = at<int>(v, v.rank, v.off.counters);
-    s_last = atomicAdd(ctr, 1) == (int)gridDim.x - 1;
-    if (s_last) *ctr = 0;  // re-armed for the next launch (graph replays)
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int w = threadIdx.x >> 5; w < E + 2 * n; w += blockDim.x >> 5) scan_row(v, w, threadIdx.x & 31);
 }
+
+// Exclusive prefix of the chunk counts, one warp per expert (and per host),
+// coalesced over the expert-major [E][C] layout; publishes the group's
+// per-expert totals into every rank's count matrix (peer stores in SPMD).
+__global__ void __launch_bounds__(256) k_route_scan(DevView v) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int E = v.E, n = v.n, C = v.C;
+  int* row;
+  if (w < E) row = at<int>(v, v.rank, v.off.chunk_hist) + (size_t)w * C;
+  else if (w < E + n) row = at<int>(v, v.rank, v.off.chunk_host) + (size_t)(w - E) * C;
+  else if (w < E + 2 * n) row = at<int>(v, v.rank, v.off.chunk_pair) + (size_t)(w - E - n) * C;
+  else return;
+  int carry = 0;
+  for (int base = 0; base < C; base += 32) {
+    const int c = base + lane;
+    const int x = (c < C) ? row[c] : 0;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (c < C) row[c] = carry + incl - x;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (w < E && lane < v.W) {
+    at<int>(v, lane, v.off.cnt_all)[v.group * E + w] = carry;
+  }
+  if (w < E && v.W > 32) {
+    for (int r = 32 + lane; r < v.W; r += 32) at<int>(v, r, v.off.cnt_all)[v.group * E + w] = carry;
+  }
+  if (w >= E + n) {  // (token, host) pair totals U[group][d], published like the counts
+    const int d = w - E - n;
+    for (int r = lane; r < v.W; r += 32) at<int>(v, r, v.off.ucnt_all)[v.group * n + d] = carry;
+  }
+}
+
 
 // Layout in one launch: every CTA rebuilds the offset tables it needs from
 // the gathered [n][E] count matrix in shared memory (a few KB), CTA 0 also
@@ -564,7 +558,11 @@ int launch_route(const DevView& v, const float* logits, const int32_t* ids,
                       (size_t)v.E * 4;
   int rc = v.elt == 8 ? launch_route_wt<double>(v, C, smem, logits, ids, w, s)
                       : launch_route_wt<float>(v, C, smem, logits, ids, w, s);
-  return rc;
+  if (rc) return rc;
+  const int warps = v.E + 2 * v.n;
+  pdl_launch(k_route_scan, (warps + 7) / 8, 256, 0, s, v);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
 }
 
 int launch_layout(const DevView& v, cudaStream_t s) {
