@@ -417,6 +417,40 @@ def run_ours(args):
         del alt_run
         alt.close()
 
+    # ---- the other layout of the same GPUs: EP only (TP1 x EP N) -- the
+    #      layout the strategy question is about (config E / SURVEY §8 a15)
+    ep_only = None
+    if world > 1 and m > 1 and not args.no_nccl:
+        xe_g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        Te = T_GLOBAL // world
+        xe = torch.randn(Te, H, device="cuda", generator=xe_g).to(torch.bfloat16)
+        le = torch.randn(Te, E, device="cuda", generator=xe_g)
+        ex2 = SwiGLUExperts.random(E, H, INTER, seed=0)
+        w13e, w2e = ex2.rank_shard(world, 1, rank)
+        del ex2
+        alt = MoELayer(world, 1, Te, H, E, K_TOP, INTER, w13=w13e, w2=w2e, rank=rank, wire="token")
+        alt_run = alt.capture(xe, le)
+        ev = []
+        for _ in range(args.steps):
+            flush.fill_(1)
+            alt.plan.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            alt_run()
+            b.record(stream)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        st = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device="cuda")
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        ep_only = {"parallelism": f"TP1xEP{world}", "wire": "token",
+                   "ms_per_step": float(st.item()),
+                   "tokens_per_s": T_GLOBAL / (float(st.item()) / 1e3)}
+        del alt_run
+        alt.close()
+        del w13e, w2e, xe, le
+        torch.cuda.empty_cache()
+
     # ---- NCCL AR + A2A baseline on the same config (N > 1)
     nccl = None
     if world > 1 and not args.no_nccl:
@@ -514,6 +548,8 @@ def run_ours(args):
             line["nccl_baseline"] = nccl
         if slot_wire is not None:
             line["wire_slot"] = slot_wire
+        if ep_only is not None:
+            line["layout_ep_only"] = ep_only
         print(json.dumps(line), flush=True)
     layer.close()
     if world > 1:
