@@ -252,7 +252,12 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
             if (i < cnt) {
               const T* pv = reinterpret_cast<const T*>(&raw[hh][i]);
 #pragma unroll
-              for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+              for (int q = 0; q < V; ++q) {
+                if constexpr (DT == MX_F64)  // reference association, uncontracted
+                  acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+                else
+                  acc[q] = fmaf(w[i], to_acc(pv[q]), acc[q]);
+              }
             }
           T out[V];
 #pragma unroll
