@@ -231,9 +231,17 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
     if wire == "token" and U is not None:
         U = np.asarray(U, dtype=np.int64)
         remote_pairs = int(U[:, group].sum() - U[group, group])
-        model["dispatch"] = {"bound": "nvlink", "bytes": remote_pairs * hb}
+        if remote_pairs > 0:
+            # pair rows arriving over NVLink (own-group rows are written
+            # straight into RECV by the same kernel, local HBM)
+            model["dispatch"] = {"bound": "nvlink", "bytes": remote_pairs * hb,
+                                 "local_hbm_bytes": T * hb + local_rows * hb}
+        else:   # one group: the dispatch is a local expert-major copy
+            model["dispatch"] = {"bound": "hbm", "bytes": T * hb + local_rows * hb}
+        # expand moves only the remote pairs: XBUF row read once, written to
+        # each of the pair's slot rows
+        model["expand"] = {"bound": "hbm", "bytes": remote_pairs * hb + remote_in * hb}
         pairs_host = int(U[:, group].sum())
-        model["expand"] = {"bound": "hbm", "bytes": pairs_host * hb + S_d * hb}
         model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * hb + pairs_host * hb}
         pull = (int(U[group].sum()) * m - int(U[group, group])) * (H // m) * 2
         model["combine"] = {"bound": "nvlink", "bytes": pull + T * H * (m - 1) // m * 2}
@@ -480,7 +488,7 @@ def run_ours(args):
     avg = {k: float(np.mean(v)) for k, v in phase_times.items()}
     rooflines = {}
     for ph, spec in model.items():
-        if ph not in avg or avg[ph] <= 0:
+        if ph not in avg or avg[ph] <= 0 or spec.get("bytes", 1) == 0:
             continue
         sec = avg[ph] / 1e3
         if spec["bound"] == "tensor":
