@@ -17,6 +17,7 @@ from .config import (CalibrationCoefficients, ClusterConfig, ConfigBundle,  # no
                      ModelHyperparams, WorkloadSpec, load_config)
 from .costmodel import (CostEstimate, indicators, lambda_ep_baseline,  # noqa: F401
                         lambda_mix)
+from .layer_model import LayerCalibration, predict_layer, select_layout  # noqa: F401
 from .plan import GateSpec  # noqa: F401
 from .skew import host_loads, host_skew, zipf_logits, zipf_popularity  # noqa: F401
 from .strategy import (ParallelStrategy, check_memory, enumerate_strategies,  # noqa: F401
@@ -33,7 +34,7 @@ __all__ = [
     "RankedStrategies", "WorkloadSpec", "calibrate", "check_memory",
     "compare_report", "enumerate_strategies", "format_strategy", "indicators",
     "lambda_ep_baseline", "lambda_mix", "load_config", "parse_strategy",
-    "select_strategy", "GateSpec", "host_loads", "host_skew", "zipf_logits", "zipf_popularity",
+    "select_strategy", "GateSpec", "LayerCalibration", "predict_layer", "select_layout", "host_loads", "host_skew", "zipf_logits", "zipf_popularity",
     "AnalyzerError", "CalibrationError", "CapacityError", "ConfigError",
     "ExpertSpec", "FP8SwiGLUExperts", "GrammarError", "MoeplanError", "RouterSpec",
     "SaturationError", "SchedulingError", "SimCluster", "StrategyError",

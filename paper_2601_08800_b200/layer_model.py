@@ -1,0 +1,149 @@
+"""Layout selection from the fused layer's own measured costs (config E).
+
+The reference selector (:mod:`.analyzer`, cm:111-153) prices MoE tensor
+parallelism as an all-reduce of ``b*s*h`` and expert parallelism as an
+all-to-all of the mean per-rank volume.  The fused B200 layer does neither:
+on one NVSwitch box it moves deduplicated (token, host) rows one hop, pre-
+reduces them per pair, and its TP sharding shrinks the grouped GEMMs' K and
+N -- which costs tensor-core efficiency the reference model cannot see.
+Measured at config B, 4 GPUs: EP4 0.331 ms vs TP2xEP2 0.366 ms on a uniform
+router, the reverse under Zipf skew (profiles/r01_configE_n4.jsonl), while
+the reference model ranks TP2xEP2 first at every skew.
+
+This module predicts the layer time of every ``(n, m)`` layout from the
+routing itself, with the same algorithmic bytes/flops ``bench.py`` reports
+per phase and per-phase efficiencies calibrated on measured bench lines:
+
+* segments separated by the layer's device barriers -- (route, layout,
+  dispatch), (expand, GEMM1, GEMM2, pair pre-reduction), (combine) -- each
+  costs its slowest rank (the barrier waits for it);
+* a phase costs ``bytes / (eff * peak)`` (HBM or NVLink) or
+  ``flops / (eff * bf16 peak)``; GEMM efficiency depends on the TP shard
+  ``I/m`` (it sets GEMM1's N and GEMM2's K);
+* route + layout and each barrier are fixed latencies.
+
+:func:`select_layout` ranks the candidate layouts; tests pin it to the
+measured config-E ordering.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["LayerCalibration", "routing_stats", "predict_layer", "select_layout"]
+
+
+@dataclass(frozen=True)
+class LayerCalibration:
+    """Peaks (MEASURED_PEAKS.json / B200_PROFILING.md) and per-phase
+    efficiencies; defaults are the round-1 B200 measurements
+    (profiles/r01_n{1,2,4}_bench.json ``rooflines``)."""
+
+    hbm_gbs: float = 6539.5
+    nvlink_gbs: float = 770.0
+    bf16_tflops: float = 1397.3
+    # GEMM efficiency vs the TP shard I/m: {I/m: (gemm1, gemm2)}
+    gemm_eff: dict = field(default_factory=lambda: {384: (0.67, 0.60), 768: (0.83, 0.73)})
+    eff: dict = field(default_factory=lambda: {
+        "dispatch_nvlink": 0.59, "dispatch_hbm": 0.86, "expand": 0.70,
+        "pair_reduce": 0.60, "combine_nvlink": 0.65, "combine_hbm": 0.63})
+    route_layout_us: float = 32.0
+    barrier_us: float = 6.0   # graph replay: ~5 us intrinsic (barrier_bench) + skew
+
+    def gemm(self, shard: int):
+        ks = sorted(self.gemm_eff)
+        if shard <= ks[0]:
+            return self.gemm_eff[ks[0]]
+        if shard >= ks[-1]:
+            return self.gemm_eff[ks[-1]]
+        for lo, hi in zip(ks, ks[1:]):
+            if lo <= shard <= hi:
+                f = (shard - lo) / (hi - lo)
+                a, b = self.gemm_eff[lo], self.gemm_eff[hi]
+                return tuple(x + f * (y - x) for x, y in zip(a, b))
+        return self.gemm_eff[ks[-1]]
+
+
+def routing_stats(ids, n: int, num_experts: int):
+    """Per-group slot and (token, host) pair counts of a routing.
+
+    ``ids``: [T_global, k] expert ids, tokens split into ``n`` contiguous
+    groups (sim:575-580), experts placed ``e*n//E`` (sim:210-212).
+    Returns ``S[j][d]`` (slots of group j hosted on d) and ``U[j][d]``
+    (tokens of group j with at least one expert on d)."""
+    ids = np.asarray(ids, dtype=np.int64)
+    Tg = ids.shape[0]
+    if Tg % n:
+        raise ValueError("tokens do not split evenly over the groups")
+    T = Tg // n
+    host = (ids * n) // num_experts
+    grp = np.repeat(np.arange(n), T)
+    S = np.zeros((n, n), dtype=np.int64)
+    U = np.zeros((n, n), dtype=np.int64)
+    for d in range(n):
+        on_d = host == d
+        S[:, d] = np.bincount(grp, weights=on_d.sum(axis=1), minlength=n).astype(np.int64)
+        U[:, d] = np.bincount(grp, weights=on_d.any(axis=1), minlength=n).astype(np.int64)
+    return S, U
+
+
+def predict_layer(ids, n: int, m: int, num_experts: int, hidden: int, inter: int,
+                  calib: LayerCalibration | None = None, elt: int = 2) -> dict:
+    """Predicted seconds per layer forward of layout ``(n, m)`` (token wire
+    for n*m > 1, slot wire on one GPU), with the per-segment breakdown."""
+    c = calib or LayerCalibration()
+    S, U = routing_stats(ids, n, num_experts)
+    Tg = np.asarray(ids).shape[0]
+    T = Tg // n
+    hb = hidden * elt
+    W = n * m
+    shard = inter // m
+    e1, e2 = c.gemm(shard)
+    hbm, nvl, tf = c.hbm_gbs * 1e9, c.nvlink_gbs * 1e9, c.bf16_tflops * 1e12
+    seg = {"pre": 0.0, "expert": 0.0, "combine": 0.0}
+    for d in range(n):
+        S_d = int(S[:, d].sum())
+        local = int(S[d, d])
+        remote_in = S_d - local
+        pairs = int(U[:, d].sum())
+        remote_pairs = pairs - int(U[d, d])
+        g1 = 2.0 * S_d * hidden * 2 * shard / (e1 * tf)
+        g2 = 2.0 * S_d * shard * hidden / (e2 * tf)
+        if W == 1:
+            disp = (T + S_d) * hb / (c.eff["dispatch_hbm"] * hbm)
+            comb = (S_d + T) * hb / (c.eff["combine_hbm"] * hbm)
+            pre, expert = disp, g1 + g2
+        else:
+            disp = max(remote_pairs * hb / (c.eff["dispatch_nvlink"] * nvl),
+                       (T + local) * hb / (c.eff["dispatch_hbm"] * hbm))
+            exp_ = (remote_pairs + remote_in) * hb / (c.eff["expand"] * hbm)
+            pr = (S_d + pairs) * hb / (c.eff["pair_reduce"] * hbm)
+            pull = (int(U[d].sum()) * m - int(U[d, d])) * (hidden // m) * elt
+            push = T * hidden * (m - 1) // m * elt
+            comb = (pull + push) / (c.eff["combine_nvlink"] * nvl)
+            pre, expert = disp, exp_ + g1 + g2 + pr
+        seg["pre"] = max(seg["pre"], pre)
+        seg["expert"] = max(seg["expert"], expert)
+        seg["combine"] = max(seg["combine"], comb)
+    fixed = c.route_layout_us * 1e-6 + (4 * c.barrier_us * 1e-6 if W > 1 else 0.0)
+    total = fixed + seg["pre"] + seg["expert"] + seg["combine"]
+    return {"layout": f"TP{m}xEP{n}", "seconds": total, "fixed_s": fixed,
+            "segments_s": seg, "host_slots_max": int(S.sum(axis=0).max())}
+
+
+def select_layout(ids, world: int, num_experts: int, hidden: int, inter: int,
+                  calib: LayerCalibration | None = None, tp_choices=(1, 2, 4, 8)):
+    """Rank the ``(n, m)`` layouts of ``world`` GPUs the expert shapes allow
+    (``(I/m) % 128 == 0``, ``n`` divides the tokens) by predicted time."""
+    Tg = np.asarray(ids).shape[0]
+    out = []
+    for m in tp_choices:
+        if world % m or (inter // m) % 128 or inter % m:
+            continue
+        n = world // m
+        if Tg % n or num_experts < n:
+            continue
+        out.append(predict_layer(ids, n, m, num_experts, hidden, inter, calib))
+    out.sort(key=lambda r: r["seconds"])
+    return out

@@ -1,0 +1,70 @@
+"""Layout selection from the fused layer's measured costs (config E).
+
+Pins :mod:`paper_2601_08800_b200.layer_model` to the round-1 B200
+measurements: the ranking of TP1xEP4 vs TP2xEP2 on 4 GPUs flips with the
+router's skew exactly as measured (profiles/r01_configE_n4.jsonl), and the
+absolute predictions stay near the measured bench lines."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2601_08800_b200.layer_model import (LayerCalibration, predict_layer,
+                                               routing_stats, select_layout)
+from paper_2601_08800_b200.skew import zipf_logits
+
+H, I, E, K, TG = 2048, 768, 128, 8, 8192
+
+
+def _ids(s, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    return torch.topk(zipf_logits(TG, E, s, seed=1, generator=g), K, dim=1).indices.numpy()
+
+
+def test_routing_stats_by_hand():
+    # 4 tokens, 2 groups of 2, 4 experts (host = e*2//4), top-2
+    ids = np.array([[0, 1], [0, 2], [3, 2], [1, 3]])
+    S, U = routing_stats(ids, 2, 4)
+    # group 0 tokens: {0,1}->host0 x2 ; {0,2}->host0,host1
+    # group 1 tokens: {3,2}->host1 x2 ; {1,3}->host0,host1
+    assert S.tolist() == [[3, 1], [1, 3]]
+    assert U.tolist() == [[2, 1], [1, 2]]
+    with pytest.raises(ValueError):
+        routing_stats(ids[:3], 2, 4)
+
+
+def test_layouts_respect_the_tp_shard_rule():
+    ids = _ids(0.0)
+    names = [r["layout"] for r in select_layout(ids, 8, E, H, I)]
+    assert set(names) == {"TP1xEP8", "TP2xEP4"}       # I/4 = 192 is not a multiple of 128
+
+
+@pytest.mark.parametrize("s,best", [(0.0, "TP1xEP4"), (0.8, "TP2xEP2"), (1.0, "TP2xEP2"),
+                                    (1.2, "TP2xEP2")])
+def test_ranking_matches_measured_config_e(s, best):
+    """Measured at 4 x B200 (round 1): EP4 0.330 ms vs TP2xEP2 0.366 ms at
+    s=0; TP2xEP2 0.384-0.388 ms vs EP4 0.403-0.424 ms for s >= 0.8."""
+    assert select_layout(_ids(s), 4, E, H, I)[0]["layout"] == best
+
+
+@pytest.mark.parametrize("n,m,measured_ms", [(1, 1, 0.702), (2, 1, 0.457), (2, 2, 0.366),
+                                             (4, 1, 0.331)])
+def test_predictions_near_measured(n, m, measured_ms):
+    # measured: bench.py lines of profiles/r01_n{1,2,4}_bench.json
+    # (value and layout_ep_only), uniform router
+    pred = predict_layer(_ids(0.0), n, m, E, H, I)["seconds"] * 1e3
+    assert abs(pred - measured_ms) / measured_ms < 0.15, pred
+
+
+def test_skew_only_hurts_expert_parallel_layouts():
+    u, z = _ids(0.0), _ids(1.2)
+    one = predict_layer(u, 1, 1, E, H, I)["seconds"]
+    assert predict_layer(z, 1, 1, E, H, I)["seconds"] == pytest.approx(one, rel=1e-9)
+    assert predict_layer(z, 4, 1, E, H, I)["seconds"] > predict_layer(u, 4, 1, E, H, I)["seconds"]
+
+
+def test_calibration_interpolates_gemm_efficiency():
+    c = LayerCalibration()
+    assert c.gemm(768) == (0.83, 0.73) and c.gemm(384) == (0.67, 0.60)
+    g1, g2 = c.gemm(576)
+    assert 0.67 < g1 < 0.83 and 0.60 < g2 < 0.73
+    assert c.gemm(192) == c.gemm(384) and c.gemm(2048) == c.gemm(768)

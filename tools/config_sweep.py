@@ -97,6 +97,7 @@ def config_e(args, rank, world, flush):
     from paper_2601_08800_b200.analyzer import calibrate, select_strategy
     from paper_2601_08800_b200.calibration import b200_cluster, measure
     from paper_2601_08800_b200.config import ModelHyperparams, WorkloadSpec
+    from paper_2601_08800_b200.layer_model import select_layout
     from paper_2601_08800_b200.strategy import format_strategy
 
     H, I, E, K = 2048, 768, 128, 8
@@ -137,6 +138,19 @@ def config_e(args, rank, world, flush):
             layer.close()
             del w13, w2
         best_meas = min(res["layouts"], key=lambda k: res["layouts"][k]["ms_per_step"])
+        # the fused-layer cost model on the EP-only layout's global routing
+        # (regenerated group by group exactly as that run drew it)
+        n_ep = world
+        T_ep = args.tokens // n_ep
+        ids_all = []
+        for g in range(n_ep):
+            gen = torch.Generator(device="cuda").manual_seed(100 + g)
+            torch.randn(T_ep, H, device="cuda", generator=gen)
+            lg_g = zipf_logits(T_ep, E, s, seed=1, device="cuda", generator=gen)
+            ids_all.append(torch.topk(lg_g, K, dim=1).indices.cpu().numpy())
+        ranked_fused = select_layout(np.concatenate(ids_all), world, E, H, I)
+        res["fused_model_pick"] = ranked_fused[0]["layout"]
+        res["fused_model_ms"] = {r["layout"]: r["seconds"] * 1e3 for r in ranked_fused}
         cl = b200_cluster(cal, 1, world)
         ranked = select_strategy(model, cl, wl, cal, expert_load=counts)
         moe = {}
