@@ -471,6 +471,38 @@ def test_wire_token_swiglu_emulated(shape):
     plan.close()
 
 
+@pytest.mark.parametrize("s_zipf,wire", [(1.2, "token"), (1.2, "slot"), (0.8, "token")])
+def test_zipf_skew_layer_emulated(s_zipf, wire):
+    """Config E on the emulated 4x2 cluster: Zipf-skewed gate logits, the
+    hot host receives far more than its share; routing counts bit-exact and
+    the layer within the bf16 tolerance of the oracle."""
+    from paper_2601_08800_b200 import SwiGLUExperts, _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    from paper_2601_08800_b200.skew import host_skew, zipf_logits
+    n, m = 4, 2
+    T, h, E, k, I = 128, 256, 32, 4, 256
+    ex = SwiGLUExperts.random(E, h, I, seed=12)
+    w13, w2 = ex.stacked_shards(n, m)
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    x = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = zipf_logits(n * T, E, s_zipf, seed=3, device="cuda", generator=gen)
+    plan = LayerPlan(n, m, T, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu", inter=I,
+                     wire=wire)
+    y = torch.empty(n * T, h, dtype=torch.bfloat16, device="cuda")
+    plan.forward(x, N.ExpertParams(None, None, w13.data_ptr(), w2.data_ptr()), logits=logits,
+                 y_out=y)
+    ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    counts = np.bincount(ids.reshape(-1), minlength=E)
+    assert host_skew(counts, n) > 1.2
+    v = plan.rank_views(0)
+    assert np.array_equal(v["exp_cnt"].cpu().numpy(), counts)
+    oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
+    assert orc.verify_metric(y.float().cpu().numpy(), y_o) <= 2e-2
+    plan.close()
+
+
 # ----------------------------------------------------------------- fp8 (config C)
 def test_quant_rows_e4m3_bit_exact():
     from paper_2601_08800_b200 import _native
