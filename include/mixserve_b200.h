@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MX_ABI_VERSION 2
+#define MX_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define MX_API __attribute__((visibility("default")))
@@ -122,8 +122,8 @@ typedef struct {
   const void* scales;
   const void* biases;
   /* MX_EXPERT_SWIGLU: this rank's TP shard of its host's experts, bf16.
-   * w13: [E/n, 2*I/tp, h] rows interleaved in blocks of 128 (gate block,
-   *      up block, ...) -- see mx_swiglu_pack_w13.
+   * w13: [E/n, 2*I/tp, h] rows interleaved in blocks of 64 (64 gate rows,
+   *      the matching 64 up rows, ...) -- see mx_swiglu_pack_w13.
    * w2:  [E/n, h, I/tp].                                                 */
   const void* w13;
   const void* w2;
@@ -232,7 +232,9 @@ MX_API int mx_baseline_combine_unpack(mx_plan* p, int rank, const void* recv,
                                void* y, void* stream);
 
 /* ----- utilities -------------------------------------------------------- */
-/* Interleave a [E_l, 2*I_t, h] gate||up shard into the w13 layout.       */
+/* Interleave [E_l, I_t, h] gate and up shards into the w13 layout:
+ * packed row 128*b + j = gate row 64*b + j, 128*b + 64 + j = up row 64*b + j.
+ * (ABI v3: the interleave was 128 rows in v2.)                            */
 MX_API int mx_swiglu_pack_w13(const void* gate, const void* up, void* w13, int E_l,
                        int I_t, int h, void* stream);
 /* Dense single-device MoE (moe_oracle, sim:302-310) on the GPU, computed

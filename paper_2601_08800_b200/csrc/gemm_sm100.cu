@@ -218,6 +218,12 @@ __device__ __forceinline__ void stage_store_chunk(unsigned char* stg, const uint
   if (lane == 0) tma_store_2d(map, stg, col, row0);
 }
 
+// w13 rows are interleaved in blocks of 64: packed row 128*b + j is gate row
+// 64*b + j, packed row 128*b + 64 + j the matching up row (mx_swiglu_pack_w13).
+// A BN-wide SwiGLU tile therefore yields BN/2 outputs; output column c of a
+// tile reads gate accumulator column swiglu_gate_col(c) and up column +64.
+__device__ __forceinline__ int swiglu_gate_col(int c) { return ((c >> 6) << 7) + (c & 63); }
+
 struct Args {
   void* D;
   const int32_t* a_rows;  // GATHER: source row of every A row (row index table)
@@ -462,17 +468,18 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (SWIGLU) {
-        // tile columns [0, BN/2) = gate, [BN/2, BN) = up (w13 interleave)
+        // gate/up accumulator columns interleaved in blocks of 64 (w13 packing)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.D) + row * args.ldd + nb * (BN / 2);
 #pragma unroll 1
         for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
+          const int gc = swiglu_gate_col(c);
           uint32_t gr[32], ur[32];
-          tmem_ld32(tbase + c, gr);
-          tmem_ld32(tbase + BN / 2 + c, ur);
+          tmem_ld32(tbase + gc, gr);
+          tmem_ld32(tbase + gc + 64, ur);
           tmem_wait_ld();
           if constexpr (FP8) {
-            scale_cols(gr, sa, args.b_scales + (size_t)bg * args.N + nb * BN + c);
-            scale_cols(ur, sa, args.b_scales + (size_t)bg * args.N + nb * BN + BN / 2 + c);
+            scale_cols(gr, sa, args.b_scales + (size_t)bg * args.N + nb * BN + gc);
+            scale_cols(ur, sa, args.b_scales + (size_t)bg * args.N + nb * BN + gc + 64);
           }
           uint32_t packed[16];
 #pragma unroll
@@ -751,9 +758,10 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.D) + row * args.ldd + nb * (BN / 2);
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
+          const int gc = swiglu_gate_col(c);
           uint32_t gr[32], ur[32];
-          tmem_ld32(tbase + c, gr);
-          tmem_ld32(tbase + BN / 2 + c, ur);
+          tmem_ld32(tbase + gc, gr);
+          tmem_ld32(tbase + gc + 64, ur);
           tmem_wait_ld();
           uint32_t packed[16];
 #pragma unroll
@@ -935,10 +943,10 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   if (M_cap < 1) return MX_OK;
   // BN = 256 unless N forbids it -- or the GEMM is weight-streaming (decode:
   // at most 64 rows per group on average), where the finer 128-column tiles
-  // spread the weight reads over more CTAs (SwiGLU needs the 256 tile: its
-  // gate/up halves are interleaved in 128-row blocks of w13)
+  // spread the weight reads over more CTAs (a 128-wide SwiGLU tile holds one
+  // 64-row gate block and its up block)
   const bool small_m = M_cap <= 64LL * G;
-  const int bn = (N % 256 == 0 && (swiglu || !small_m)) ? 256 : 128;
+  const int bn = (N % 256 == 0 && !small_m) ? 256 : 128;
   CUtensorMap ma, mb, md;
   memset(&md, 0, sizeof(md));
   const bool gather = a_rows != nullptr;
@@ -964,7 +972,8 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   if (gather) {
     if (bn == 256) return swiglu ? launch<256, true, true>(ma, mb, md, a, max_tiles, s)
                                  : launch<256, false, true>(ma, mb, md, a, max_tiles, s);
-    return launch<128, false, true>(ma, mb, md, a, max_tiles, s);
+    return swiglu ? launch<128, true, true>(ma, mb, md, a, max_tiles, s)
+                  : launch<128, false, true>(ma, mb, md, a, max_tiles, s);
   }
   if (bn == 256 && out_dtype == MX_BF16 && use_pair(G, M_total)) {
     // CTA-pair kernel: A box 128 rows (each CTA its half of the 256-row tile),
@@ -978,7 +987,8 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   }
   if (bn == 256) return swiglu ? launch<256, true, false>(ma, mb, md, a, max_tiles, s)
                                : launch<256, false, false>(ma, mb, md, a, max_tiles, s);
-  return launch<128, false, false>(ma, mb, md, a, max_tiles, s);
+  return swiglu ? launch<128, true, false>(ma, mb, md, a, max_tiles, s)
+                : launch<128, false, false>(ma, mb, md, a, max_tiles, s);
 }
 
 // e4m3 x e4m3 -> f32 grouped GEMM with per-row activation scales (fp32 at

@@ -10,8 +10,8 @@ __global__ void k_pack_w13(const __nv_bfloat16* gate, const __nv_bfloat16* up, _
   const long long rows = (long long)E_l * 2 * I_t;
   for (long long rr = blockIdx.x; rr < rows; rr += gridDim.x) {
     const int e = (int)(rr / (2 * I_t)), r = (int)(rr % (2 * I_t));
-    const int b = r / 256, q = r % 256;
-    const __nv_bfloat16* src = (q < 128 ? gate : up) + ((size_t)e * I_t + b * 128 + (q & 127)) * h;
+    const int b = r / 128, q = r % 128;  // blocks of 64 gate rows, then 64 up rows
+    const __nv_bfloat16* src = (q < 64 ? gate : up) + ((size_t)e * I_t + b * 64 + (q & 63)) * h;
     __nv_bfloat16* dst = w13 + (size_t)rr * h;
     for (int c = threadIdx.x; c < h; c += blockDim.x) dst[c] = src[c];
   }

@@ -341,7 +341,7 @@ class FP8SwiGLUExperts:
             w13 = (p["w13"].float() * p["w13_scale"][..., None]).cpu().numpy()
             w2 = (p["w2"].float() * p["w2_scale"][..., None]).cpu().numpy()
             for i in range(w13.shape[0]):
-                blocks = w13[i].reshape(-1, 2, 128, self.h)
+                blocks = w13[i].reshape(-1, 2, 64, self.h)
                 gate[e0 + i, t] = blocks[:, 0].reshape(It, self.h)
                 up[e0 + i, t] = blocks[:, 1].reshape(It, self.h)
                 down[e0 + i, t] = w2[i]
@@ -352,7 +352,7 @@ class FP8SwiGLUExperts:
                           np.zeros((m, Ist, self.h), np.float32),
                           np.zeros((m, self.h, Ist), np.float32)]
                 s13 = (p["w13_shared"].float() * p["w13_shared_scale"][..., None]).cpu().numpy()
-                blocks = s13.reshape(-1, 2, 128, self.h)
+                blocks = s13.reshape(-1, 2, 64, self.h)
                 sh[0][t] = blocks[:, 0].reshape(-1, self.h)
                 sh[1][t] = blocks[:, 1].reshape(-1, self.h)
                 sh[2][t] = (p["w2_shared"].float() * p["w2_shared_scale"][..., None]).cpu().numpy()

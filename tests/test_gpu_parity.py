@@ -291,13 +291,15 @@ def test_grouped_gemm_vs_torch_fp32(G, N, K, out):
     assert torch.all(D[M:].float() == 7.0)   # rows past the groups untouched
 
 
-def test_grouped_gemm_swiglu_epilogue():
+@pytest.mark.parametrize("counts", [(130, 0, 64), (5, 0, 9)])  # 256- and 128-wide tiles
+def test_grouped_gemm_swiglu_epilogue(counts):
     from paper_2601_08800_b200 import _native
     G, I, K = 3, 256, 256
     gen = torch.Generator(device="cuda").manual_seed(1)
-    cnts = torch.tensor([130, 0, 64], dtype=torch.int32)
-    offs = torch.tensor([0, 130, 130], dtype=torch.int32)
-    M = 194
+    cnts = torch.tensor(counts, dtype=torch.int32)
+    offs = torch.zeros(G, dtype=torch.int32)
+    offs[1:] = torch.cumsum(cnts, 0)[:-1]
+    M = int(cnts.sum())
     A = torch.randn(M, K, device="cuda", generator=gen).to(torch.bfloat16)
     wg = (torch.randn(G, I, K, device="cuda", generator=gen) / 16).to(torch.bfloat16)
     wu = (torch.randn(G, I, K, device="cuda", generator=gen) / 16).to(torch.bfloat16)
@@ -554,8 +556,8 @@ def test_grouped_gemm_fp8_vs_dequantized_torch(swiglu):
             continue
         ref = (aq[o:o + c] * asc[o:o + c, None]) @ (Bq[g].float() * ws[g][:, None]).T
         if swiglu:
-            # w13 interleave: per 256-row block, 128 gate rows then 128 up rows
-            blocks = ref.view(c, N // 256, 2, 128)
+            # w13 interleave: per 128-row block, 64 gate rows then 64 up rows
+            blocks = ref.view(c, N // 128, 2, 64)
             ref = (torch.nn.functional.silu(blocks[:, :, 0]) * blocks[:, :, 1]).reshape(c, N // 2)
         got = D[o:o + c].float()
         assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (g, (got - ref).abs().max())

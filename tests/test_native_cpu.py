@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), f"{s} declared in include/ but not exported"
         assert s in N.SIGNATURES or s == "mx_last_error"
-    assert lib.mx_abi_version() == 2
+    assert lib.mx_abi_version() == 3
 
 
 def test_plan_heap_bytes_and_validation_map_to_reference_errors():
