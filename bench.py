@@ -520,9 +520,11 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(sample_tokens=args.cpu_sample)
 
-    # gate, route, scan, layout, dispatch, gemm1, gemm2, combine (+4 barriers;
-    # +expand, +pair_reduce for wire TOKEN) -- profiles/r01b_n1_launches.csv
-    launches_per_step = 8 + (4 if world > 1 else 0) + (2 if wire == "token" else 0)
+    # gate, route, scan, layout, dispatch, gemm1, gemm2, combine (+3 barriers,
+    # +1 TP-group barrier when m > 1; +expand, +pair_reduce for wire TOKEN)
+    # -- profiles/r01_n1_launches.csv
+    launches_per_step = (8 + ((4 if m > 1 else 3) if world > 1 else 0)
+                         + (2 if wire == "token" else 0))
     if rank == 0:
         line = {
             "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",

@@ -651,8 +651,9 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
   if ((rc = mx_combine(p, rank, nullptr, stream))) return rc;
   // y complete: every TP peer of the group pushed its shard.  Group-local --
   // nothing of another group is touched before the next forward's first
-  // full barrier (its route only writes count rows read after that barrier)
-  if ((rc = barrier(p, s, true))) return rc;
+  // full barrier (its route only writes count rows read after that barrier);
+  // without TP peers (m == 1) y is written by this rank alone: no barrier
+  if (p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;
   if (y_out) {
     RankIter it;
     if ((rc = ranks_for(p, rank, &it))) return rc;
