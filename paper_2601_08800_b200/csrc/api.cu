@@ -216,6 +216,8 @@ struct mx_plan {
   // by the baseline's unpack, which materialises RECV instead)
   const void* a_src[MX_MAXW] = {};
   long long a_src_rows[MX_MAXW] = {};
+  // fused device barrier flags for the next phase (mx_forward, SPMD only)
+  int sync_signal = 0, sync_wait = 0;
 };
 
 static DevView view_for(const mx_plan* p, int r) {
@@ -225,6 +227,8 @@ static DevView view_for(const mx_plan* p, int r) {
   v.tp_rank = r % p->d.tp;
   v.a_src = p->a_src[r];
   v.a_src_rows = p->a_src_rows[r];
+  v.sync_signal = p->sync_signal;
+  v.sync_wait = p->sync_wait;
   return v;
 }
 
@@ -567,9 +571,16 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
   for (int r = it.first; r < it.last; ++r) {
     DevView v = view_for(p, r);
     const bool tok = p->d.wire == MX_WIRE_TOKEN;
+    // fused barrier (stage 0 only): the stage's first kernel waits, its last
+    // one signals -- expand / pair_reduce on the token wire, else the
+    // expert kernels themselves
+    DevView vfirst = v, vlast = v;
+    vfirst.sync_signal = 0;
+    vlast.sync_wait = 0;
+    if (tok) v.sync_wait = v.sync_signal = 0;
     if (tok && (stage == 0 || stage == 3)) {
       // gathered GEMM1 only needs the row table; otherwise expand into RECV
-      rc = v.a_src ? launch_rowsrc_token(v, s) : launch_expand(v, s);
+      rc = v.a_src ? launch_rowsrc_token(vfirst, s) : launch_expand(vfirst, s);
       if (rc) return rc;
     }
     if (stage == 3 || stage == 4) {
@@ -604,7 +615,7 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
                                 static_cast<const char*>(ep->w2) + slot * w2_rank, stage, s);
     }
     if (rc) return rc;
-    if (tok && stage == 0 && (rc = launch_pair_reduce(v, s))) return rc;
+    if (tok && stage == 0 && (rc = launch_pair_reduce(vlast, s))) return rc;
   }
   return MX_OK;
 }
@@ -637,23 +648,71 @@ int mx_combine(mx_plan* p, int rank, void* y_out, void* stream) {
   return MX_OK;
 }
 
+// Optionally (MX_FUSE_BARRIER_T = max tokens per group, default 0 = off) the
+// inter-phase barriers are folded into the phase kernels (SPMD, W > 1, every
+// phase guaranteed to launch on every rank): the producer's last CTA
+// publishes the epoch, the consumer's CTAs wait for it at entry, combine's
+// last CTA publishes and waits (y complete, buffers reusable).  Measured on
+// B200 it is slower than the standalone barrier kernels at every size --
+// config B N=4 prefill 0.442 vs 0.395 ms, decode T_g=64 162.6 vs 143.0 us --
+// per-CTA system-scope fences and every CTA polling peer flags cost more
+// than the launches they save.  Kept opt-in for persistent-kernel work.
+static bool fused_barriers(const mx_plan* p) {
+  static const long long limit = [] {
+    const char* e = getenv("MX_FUSE_BARRIER_T");
+    return e ? atoll(e) : 0LL;
+  }();
+  const mx_comm* c = p->comm;
+  return !c->emulate && c->W > 1 && p->d.tokens > 0 && p->d.tokens <= limit && p->cap >= 1 &&
+         p->d.num_experts >= p->d.n_group && !gathers(p);
+}
+
+namespace {
+struct SyncFlags {  // sets the plan's fused-barrier flags for one phase
+  mx_plan* p;
+  SyncFlags(mx_plan* p_, bool on, int wait, int sig) : p(p_) {
+    p->sync_wait = on ? wait : 0;
+    p->sync_signal = on ? sig : 0;
+  }
+  ~SyncFlags() { p->sync_wait = p->sync_signal = 0; }
+};
+}  // namespace
+
 int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const int32_t* ids,
                const void* weights, const mx_expert_params* ep, void* y_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool fuse = fused_barriers(p);
   int rc;
-  if ((rc = mx_route(p, rank, logits, ids, weights, stream))) return rc;
-  if ((rc = barrier(p, s))) return rc;            // every group's counts published
-  if ((rc = mx_layout(p, rank, 0, stream))) return rc;
-  if ((rc = mx_dispatch(p, rank, x, stream))) return rc;
-  if ((rc = barrier(p, s))) return rc;            // every row landed
-  if ((rc = mx_expert(p, rank, ep, stream))) return rc;
-  if ((rc = barrier(p, s))) return rc;            // every partial written
-  if ((rc = mx_combine(p, rank, nullptr, stream))) return rc;
+  {
+    SyncFlags f(p, fuse, 0, 1);
+    if ((rc = mx_route(p, rank, logits, ids, weights, stream))) return rc;
+  }
+  if (!fuse && (rc = barrier(p, s))) return rc;  // every group's counts published
+  {
+    SyncFlags f(p, fuse, 1, 0);
+    if ((rc = mx_layout(p, rank, 0, stream))) return rc;
+  }
+  {
+    SyncFlags f(p, fuse, 0, 1);
+    if ((rc = mx_dispatch(p, rank, x, stream))) return rc;
+  }
+  if (!fuse && (rc = barrier(p, s))) return rc;  // every row landed
+  {
+    SyncFlags f(p, fuse, 1, 1);
+    if ((rc = mx_expert(p, rank, ep, stream))) return rc;
+  }
+  if (!fuse && (rc = barrier(p, s))) return rc;  // every partial written
+  {
+    // the combine's closing publish-and-wait makes y complete; without TP
+    // peers (m == 1) this rank wrote all of y itself
+    SyncFlags f(p, fuse, 1, p->d.tp > 1 ? 1 : 0);
+    if ((rc = mx_combine(p, rank, nullptr, stream))) return rc;
+  }
   // y complete: every TP peer of the group pushed its shard.  Group-local --
   // nothing of another group is touched before the next forward's first
   // full barrier (its route only writes count rows read after that barrier);
   // without TP peers (m == 1) y is written by this rank alone: no barrier
-  if (p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;
+  if (!fuse && p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;
   if (y_out) {
     RankIter it;
     if ((rc = ranks_for(p, rank, &it))) return rc;

@@ -22,6 +22,7 @@ namespace mx {
 template <int DT, bool VEC, int KU>
 __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);  // every host's partials are written
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = VEC ? Elt<DT>::V : 1;  // elements per 16 B vector
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
     }
     __syncwarp();
   }
+  if (v.sync_signal) grid_signal_and_wait(v);  // y complete on every TP rank: barrier #4
 }
 
 template <int DT>

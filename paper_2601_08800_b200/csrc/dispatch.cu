@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) k_dispatch(DevView v, const char* __restr
       }
     }
   }
+  if (v.sync_signal) grid_signal(v);  // rows landed (fused barrier)
 }
 
 // Token-major form for rows of at most VPL x 512 B: warp per token, the row
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(256) k_dispatch_rows(DevView v, const char* __
       }
     }
   }
+  if (v.sync_signal) grid_signal(v);  // rows landed (fused barrier)
 }
 
 int launch_dispatch(const DevView& v, const void* x, cudaStream_t s) {

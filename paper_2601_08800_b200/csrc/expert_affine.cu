@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(256)
 k_expert_affine(DevView v, const typename Elt<DT>::Acc* __restrict__ scales,
                 const typename Elt<DT>::Acc* __restrict__ biases) {
   pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);  // fused barrier: every peer's rows have landed
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   __shared__ int s_off[MX_EMAX + 1];
@@ -44,6 +45,7 @@ k_expert_affine(DevView v, const typename Elt<DT>::Acc* __restrict__ scales,
     val = add_rn(val, biases[e] / m);
     part[idx] = from_acc<T>(val);
   }
+  if (v.sync_signal) grid_signal(v);
 }
 
 int launch_expert_affine(const DevView& v, const void* scales, const void* biases,

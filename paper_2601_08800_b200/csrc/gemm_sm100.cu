@@ -230,6 +230,8 @@ struct Args {
   const char* a_base;     // FP8: A rows (lda bytes each), fp32 row scale at byte K
   long long lda;          // FP8: A row stride in bytes
   const float* b_scales;  // FP8: per-B-row (output channel) scales, [G*N]
+  int sync_wait, sync_signal;  // fused device barrier (SPMD forward)
+  DevView sv;                  // rank view for the fused barrier
   const int32_t* offs;
   const int32_t* cnts;
   const int32_t* b_index;
@@ -279,6 +281,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   // group offsets/counts -> smem (parallel loads), then the per-group tile
   // prefix by one warp-scan pass (G <= MX_EMAX); no per-tile global reads
   pdl_wait();  // group offsets/counts and A are written by earlier kernels
+  if (args.sync_wait) grid_wait(args.sv);  // peers' rows have landed
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     s_off[g] = args.offs[g];
     s_cnt[g] = args.cnts[g];
@@ -539,7 +542,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) tma_store_wait_all();
+    if (lane == 0) {
+      tma_store_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
   }
 
   tc_fence_before();
@@ -549,6 +555,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(C::TMEM_COLS));
   }
+  if (args.sync_signal) grid_signal(args.sv);  // D complete (bulk stores drained): publish
 }
 
 // ------------------------------------------------------------ CTA pair (2SM)
@@ -636,6 +643,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   pdl_wait();  // group offsets/counts and A are written by earlier kernels
+  if (args.sync_wait) grid_wait(args.sv);  // peers' rows have landed
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     s_off[g] = args.offs[g];
     s_cnt[g] = args.cnts[g];
@@ -811,7 +819,10 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);  // leader's tempty[acc]
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) tma_store_wait_all();
+    if (lane == 0) {
+      tma_store_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
   }
 
   tc_fence_before();
@@ -821,6 +832,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
+  if (args.sync_signal) grid_signal(args.sv);
 }
 
 // ------------------------------------------------------------ host side
@@ -934,7 +946,7 @@ static bool use_pair(int G, long long M_total) {
 int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,
                  const int32_t* cnts, const int32_t* b_index, int G, long long M_total,
                  long long M_cap, int N, int K, int swiglu, cudaStream_t s,
-                 const int32_t* a_rows, long long a_src_rows) {
+                 const int32_t* a_rows, long long a_src_rows, const DevView* sync) {
   using namespace gemm;
   if (G < 1 || G > MX_EMAX) { set_error("grouped_gemm: G=%d outside [1, %d]", G, MX_EMAX); return MX_ERR_UNSUPPORTED; }
   if (K % BK != 0 || N % 128 != 0) { set_error("grouped_gemm: K %% 64 and N %% 128 must be 0 (K=%d N=%d)", K, N); return MX_ERR_UNSUPPORTED; }
@@ -963,6 +975,7 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
     if (rc) return rc;
   }
   Args a{};
+  if (sync) { a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal; }
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
@@ -997,7 +1010,8 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
 // sum_k (qa*sa) (qb*sb) exactly as the CPU replica computes it.
 int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b_scales, void* D,
                      const int32_t* offs, const int32_t* cnts, const int32_t* b_index, int G,
-                     long long M_total, long long M_cap, int N, int K, int swiglu, cudaStream_t s) {
+                     long long M_total, long long M_cap, int N, int K, int swiglu, cudaStream_t s,
+                     const DevView* sync) {
   using namespace gemm;
   if (G < 1 || G > MX_EMAX) { set_error("grouped_gemm_fp8: G=%d outside [1, %d]", G, MX_EMAX); return MX_ERR_UNSUPPORTED; }
   if (K % 128 != 0 || N % 256 != 0) { set_error("grouped_gemm_fp8: K %% 128 and N %% 256 must be 0 (K=%d N=%d)", K, N); return MX_ERR_UNSUPPORTED; }
@@ -1011,6 +1025,7 @@ int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b
   rc = make_map(&md, D, M_cap, swiglu ? N / 2 : N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
   Args a{};
+  if (sync) { a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal; }
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index;
   a.a_base = static_cast<const char*>(A); a.lda = lda; a.b_scales = b_scales;
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = 0;
@@ -1031,21 +1046,28 @@ int launch_expert_fp8(const DevView& v, const mx_expert_params& ep, int stage, c
   const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
   const int32_t* sh = at<int32_t>(v, v.rank, v.off.sh_meta);
   const int* host_rows = at<int>(v, v.rank, v.off.host_rows) + v.group;
+  const bool shared = v.Is_t && v.T > 0;
+  // fused barrier: the first GEMM of the stage waits, the last one signals
+  DevView first = v, last = v, none = v;
+  first.sync_signal = 0;
+  last.sync_wait = 0;
+  none.sync_wait = none.sync_signal = 0;
+  const bool routed_first = El > 0;
   int rc = MX_OK;
   if (stage != 2) {
     if (El > 0) {
       rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.recv), v.wrow, ep.w13, ep.w13_scale,
                             at<char>(v, v.rank, v.off.act), offs, cnts, nullptr, El, v.cap, v.cap,
-                            2 * v.I_t, v.h, 1, s);
+                            2 * v.I_t, v.h, 1, s, &first);
       if (rc) return rc;
       rc = quant_rows_e4m3(at<char>(v, v.rank, v.off.act), v.I_t, at<char>(v, v.rank, v.off.actq),
                            v.I_t + 16, v.cap, host_rows, v.I_t, s);
       if (rc) return rc;
     }
-    if (v.Is_t && v.T > 0) {
+    if (shared) {
       rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.xq), v.wrow, ep.w13_shared, ep.w13_shared_scale,
                             at<char>(v, v.rank, v.off.act_s), sh, sh + 1, nullptr, 1, v.T, v.T,
-                            2 * v.Is_t, v.h, 1, s);
+                            2 * v.Is_t, v.h, 1, s, routed_first ? &none : &first);
       if (rc) return rc;
       rc = quant_rows_e4m3(at<char>(v, v.rank, v.off.act_s), v.Is_t,
                            at<char>(v, v.rank, v.off.actq_s), v.Is_t + 16, v.T, nullptr, v.Is_t, s);
@@ -1056,13 +1078,13 @@ int launch_expert_fp8(const DevView& v, const mx_expert_params& ep, int stage, c
     if (El > 0) {
       rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.actq), v.I_t + 16, ep.w2, ep.w2_scale,
                             at<char>(v, v.rank, v.off.partial), offs, cnts, nullptr, El, v.cap,
-                            v.cap, v.h, v.I_t, 0, s);
+                            v.cap, v.h, v.I_t, 0, s, shared ? &none : &last);
       if (rc) return rc;
     }
-    if (v.Is_t && v.T > 0) {
+    if (shared) {
       rc = grouped_gemm_fp8(at<char>(v, v.rank, v.off.actq_s), v.Is_t + 16, ep.w2_shared,
                             ep.w2_shared_scale, at<char>(v, v.rank, v.off.part_s), sh, sh + 1,
-                            nullptr, 1, v.T, v.T, v.h, v.Is_t, 0, s);
+                            nullptr, 1, v.T, v.T, v.h, v.Is_t, 0, s, &last);
       if (rc) return rc;
     }
   }
@@ -1077,17 +1099,21 @@ int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int 
   if (El == 0) return MX_OK;
   const int32_t* offs = at<int32_t>(v, v.rank, v.off.exp_off) + e0;
   const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
+  DevView first = v, last = v;  // fused barrier: GEMM1 waits, GEMM2 signals
+  first.sync_signal = 0;
+  last.sync_wait = 0;
   if (stage != 2) {
     // GEMM1 A operand: gathered token rows (row table + source buffer) when
     // the layout provides them, else the materialised expert-major RECV
     const void* A = v.a_src ? v.a_src : at<char>(v, v.rank, v.off.recv);
     const int32_t* rows = v.a_src ? at<int32_t>(v, v.rank, v.off.recv_src) : nullptr;
     int rc = grouped_gemm(A, w13, at<char>(v, v.rank, v.off.act), MX_BF16, offs, cnts, nullptr, El,
-                          v.cap, v.cap, 2 * v.I_t, v.h, 1, s, rows, v.a_src_rows);
+                          v.cap, v.cap, 2 * v.I_t, v.h, 1, s, rows, v.a_src_rows, &first);
     if (rc || stage == 1) return rc;
   }
   return grouped_gemm(at<char>(v, v.rank, v.off.act), w2, at<char>(v, v.rank, v.off.partial),
-                      MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s, nullptr, 0);
+                      MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s, nullptr, 0,
+                      &last);
 }
 
 }  // namespace mx

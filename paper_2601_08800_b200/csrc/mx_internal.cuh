@@ -96,6 +96,8 @@ struct DevView {
   int wrow;           // bytes per row on the wire (h*welt [+16 scale tail])
   int fp8;            // SWIGLU_FP8 plan
   int Is_t;           // shared expert intermediate per TP rank (0: none)
+  int sync_signal;    // fused barrier: this kernel's last CTA publishes the epoch
+  int sync_wait;      // fused barrier: every CTA waits for all peers' epoch at entry
   const void* a_src;  // GEMM1 gathers A rows from here (x or XBUF), nullptr: RECV
   long long a_src_rows;
   long long cap;
@@ -175,6 +177,66 @@ inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// ---------------------------------------------------------------- fused barriers
+// The device barrier between phases, folded into the kernels (SPMD, W > 1):
+// the producer kernel's last CTA to finish bumps the rank's epoch and
+// publishes it to every peer's flag slot (release, system scope); the
+// consumer kernel's CTAs wait at entry until every peer published it.  The
+// epoch counter is the same one k_barrier uses, so fused and standalone
+// barriers interleave consistently.  Watchdog: error flag, no hang.
+__device__ __forceinline__ unsigned long long* epoch_ctr(const DevView& v) {
+  return reinterpret_cast<unsigned long long*>(reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 2);
+}
+__device__ __forceinline__ void grid_signal(const DevView& v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    int* ctr = reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 4;
+    if (atomicAdd(ctr, 1) == (int)(gridDim.x * gridDim.y) - 1) {
+      __threadfence_system();
+      *ctr = 0;
+      const unsigned long long e = ++(*epoch_ctr(v));
+      for (int r = 0; r < v.W; ++r)
+        st_release_sys(reinterpret_cast<unsigned long long*>(v.heap[r] + v.off.flags) + v.rank, e);
+    }
+  }
+}
+__device__ __forceinline__ void grid_wait(const DevView& v) {
+  if ((int)threadIdx.x < v.W) {
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(epoch_ctr(v));
+    const unsigned long long* mine =
+        reinterpret_cast<const unsigned long long*>(v.heap[v.rank] + v.off.flags) + threadIdx.x;
+    const long long t0 = clock64();
+    while (ld_acquire_sys(mine) < e) {
+      if (clock64() - t0 > 20000000000LL) {
+        atomicOr(reinterpret_cast<int*>(v.heap[v.rank] + v.off.err) + 2, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+// combine's tail: publish, then the last CTA waits for every peer, so the
+// kernel completes only when every TP peer's output shard has landed
+__device__ __forceinline__ void grid_signal_and_wait(const DevView& v) {
+  __syncthreads();
+  __shared__ int s_is_last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    int* ctr = reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 4;
+    s_is_last = atomicAdd(ctr, 1) == (int)(gridDim.x * gridDim.y) - 1;
+    if (s_is_last) {
+      __threadfence_system();
+      *ctr = 0;
+      const unsigned long long e = ++(*epoch_ctr(v));
+      for (int r = 0; r < v.W; ++r)
+        st_release_sys(reinterpret_cast<unsigned long long*>(v.heap[r] + v.off.flags) + v.rank, e);
+    }
+  }
+  __syncthreads();
+  if (s_is_last) grid_wait(v);
+}
+
 // ---------------------------------------------------------------- dtypes
 template <int DT> struct Elt;
 template <> struct Elt<MX_F64> { using T = double; using Acc = double; static constexpr int V = 2; };
@@ -229,10 +291,12 @@ int launch_baseline_combine_unpack(const DevView& v, const void* recv, void* y,
 int grouped_gemm(const void* A, const void* B, void* D, int out_dtype,
                  const int32_t* offs, const int32_t* cnts, const int32_t* b_index,
                  int G, long long M_total, long long M_cap, int N, int K, int swiglu,
-                 cudaStream_t s, const int32_t* a_rows = nullptr, long long a_src_rows = 0);
+                 cudaStream_t s, const int32_t* a_rows = nullptr, long long a_src_rows = 0,
+                 const DevView* sync = nullptr);
 int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b_scales, void* D,
                      const int32_t* offs, const int32_t* cnts, const int32_t* b_index, int G,
-                     long long M_total, long long M_cap, int N, int K, int swiglu, cudaStream_t s);
+                     long long M_total, long long M_cap, int N, int K, int swiglu, cudaStream_t s,
+                     const DevView* sync = nullptr);
 int quant_rows_e4m3(const void* src, long long lds, void* dst, long long ldd, long long rows,
                     const int32_t* rows_dev, int cols, cudaStream_t s);
 int launch_rowsrc_slot(const DevView& v, cudaStream_t s);

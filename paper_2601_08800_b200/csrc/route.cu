@@ -353,13 +353,12 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int E = v.E, n = v.n, C = v.C;
-  int* row;
+  int* row = nullptr;
   if (w < E) row = at<int>(v, v.rank, v.off.chunk_hist) + (size_t)w * C;
   else if (w < E + n) row = at<int>(v, v.rank, v.off.chunk_host) + (size_t)(w - E) * C;
   else if (w < E + 2 * n) row = at<int>(v, v.rank, v.off.chunk_pair) + (size_t)(w - E - n) * C;
-  else return;
   int carry = 0;
-  for (int base = 0; base < C; base += 32) {
+  for (int base = 0; row && base < C; base += 32) {
     const int c = base + lane;
     const int x = (c < C) ? row[c] : 0;
     int incl = x;
@@ -377,10 +376,11 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
   if (w < E && v.W > 32) {
     for (int r = 32 + lane; r < v.W; r += 32) at<int>(v, r, v.off.cnt_all)[v.group * E + w] = carry;
   }
-  if (w >= E + n) {  // (token, host) pair totals U[group][d], published like the counts
+  if (row && w >= E + n) {  // (token, host) pair totals U[group][d], published like the counts
     const int d = w - E - n;
     for (int r = lane; r < v.W; r += 32) at<int>(v, r, v.off.ucnt_all)[v.group * n + d] = carry;
   }
+  if (v.sync_signal) grid_signal(v);  // counts published: barrier #1
 }
 
 
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
 // and every (token, host) pair row.
 __global__ void __launch_bounds__(512) k_layout(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);  // every group's counts have landed
   extern __shared__ int sm[];
   const int n = v.n, E = v.E, k = v.k, j = v.group;
   int* s_cnt = sm;                   // [n][E]

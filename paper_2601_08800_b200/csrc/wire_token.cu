@@ -86,17 +86,23 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
         }
         const unsigned mine = __ballot_sync(0xffffffffu, pos >= 0);
         char* recv = at<char>(v, v.rank, v.off.recv);
-        for (size_t i = r_lo + lane; i < r_hi; i += 128) {
+        // warp-uniform passes (the slot broadcast below is a full-warp
+        // shuffle), each lane predicated on its own vectors
+        for (size_t base = r_lo; base < r_hi; base += 128) {
           uint4 val[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (i + 32 * q < r_hi) val[q] = ld_v4(row + ((i + 32 * q) << 4));
+          for (int q = 0; q < 4; ++q) {
+            const size_t i = base + lane + 32 * q;
+            if (i < r_hi) val[q] = ld_v4(row + (i << 4));
+          }
           for (unsigned b = mine; b; b &= b - 1) {
             const int p = __shfl_sync(0xffffffffu, pos, __ffs(b) - 1);
             char* dst = recv + (size_t)p * row_bytes;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (i + 32 * q < r_hi) st_v4(dst + ((i + 32 * q) << 4), val[q]);
+            for (int q = 0; q < 4; ++q) {
+              const size_t i = base + lane + 32 * q;
+              if (i < r_hi) st_v4(dst + (i << 4), val[q]);
+            }
           }
         }
       } else if (d == v.group) {
@@ -156,6 +162,7 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
       if (idx == 0) at<int>(v, dst, v.off.pair_n)[u] = cnt;
     }
   }
+  if (v.sync_signal) grid_signal(v);  // rows + pair lists landed: barrier #2
 }
 
 // Host side: expert-major RECV rows from the deduplicated XBUF (local HBM),
@@ -164,6 +171,7 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
 template <class WT>
 __global__ void __launch_bounds__(256) k_expand(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -283,6 +291,7 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
       st_v4(z + (size_t)u * h + c, *reinterpret_cast<uint4*>(out));
     }
   }
+  if (v.sync_signal) grid_signal(v);  // z written: barrier #3
 }
 
 // Owner (j, t): y[tok, cols t] = sum over hosts (j-1, ..., j) and TP ranks
@@ -290,6 +299,7 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
 template <int DT>
 __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);  // every host's z is written
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
@@ -397,6 +407,7 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
         st_v4(at<T>(v, j * m + tt, v.off.y) + (size_t)t * h + c, *reinterpret_cast<uint4*>(out));
     }
   }
+  if (v.sync_signal) grid_signal_and_wait(v);  // y complete on every TP rank: barrier #4
 }
 
 // Gathered GEMM1 (SwiGLU): the row table replaces the expansion copy --
@@ -404,6 +415,7 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
 template <class WT>
 __global__ void k_rowsrc_token(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);
   const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
