@@ -39,6 +39,19 @@ NVLINK_PEER_GBS = 770.0      # measured peer copy, B200_PROFILING.md
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+OUT = sys.stdout  # the JSON line's stream (see json_stdout)
+
+
+def json_stdout():
+    """Keep the process's stdout to the one JSON line: file descriptor 1 is
+    routed to stderr (NCCL / c10d / library banners included) and the
+    returned file writes to the original stdout."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return out
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -196,7 +209,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=OUT, flush=True)
 
 
 # ------------------------------------------------------------------ ours
@@ -560,7 +573,7 @@ def run_ours(args):
             line["wire_slot"] = slot_wire
         if ep_only is not None:
             line["layout_ep_only"] = ep_only
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=OUT, flush=True)
     layer.close()
     if world > 1:
         dist.barrier()
@@ -589,10 +602,13 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
+    global OUT
+    OUT = json_stdout()
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
+    OUT.flush()
 
 
 if __name__ == "__main__":
