@@ -28,9 +28,9 @@ __device__ __forceinline__ float warp_max_f32(float v) {
 // Fused softmax + top-k gate: one warp per token over all SMs.  Lane owns
 // experts e = 128*i + 4*lane + q (128-bit coalesced row loads).  Selection
 // key: fp32 logit descending, lowest id on ties (exact compares, so ids are
-// bit-exact with the oracle).  Each lane caches its best untaken candidate;
-// only the winning lane rescans.  A round is two warp reductions: the max
-// key (redux.sync.max.f32) and the lowest id holding it (redux.sync.min).
+// bit-exact with the oracle).  Each lane sorts its candidates once; a round
+// is two warp reductions -- the max key (redux.sync.max.f32) and the lowest
+// id holding it (redux.sync.min) -- and a pop of the winning lane's list.
 template <class WT, int EV>
 __global__ void __launch_bounds__(256)
 k_gate(DevView v, const float* __restrict__ logits) {
@@ -54,49 +54,62 @@ k_gate(DevView v, const float* __restrict__ logits) {
       for (int q = 0; q < 4; ++q) val[4 * i + q] = (e0 + q < E) ? __ldg(row + e0 + q) : -INFINITY;
     }
   }
-  unsigned taken = 0;
-  float cv;
-  int ce;
-  auto rescan = [&]() {
-    cv = -INFINITY;
-    ce = 0x7fffffff;
+  // each lane sorts its candidates once (key descending, lowest id first on
+  // ties); a round then only advances the winning lane's list
+  constexpr int NV = EV * 4;
+  int se[NV];
 #pragma unroll
-    for (int i = 0; i < EV * 4; ++i) {
-      const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
-      if (e < E && !((taken >> i) & 1u) && (val[i] > cv || (val[i] == cv && e < ce))) {
-        cv = val[i];
-        ce = e;
-      }
+  for (int i = 0; i < NV; ++i) {
+    const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
+    se[i] = e < E ? e : 0x7fffffff;
+    if (e >= E) val[i] = -INFINITY;
+  }
+#pragma unroll
+  for (int i = 1; i < NV; ++i) {
+#pragma unroll
+    for (int j = i; j > 0; --j) {
+      const bool before = val[j] > val[j - 1] || (val[j] == val[j - 1] && se[j] < se[j - 1]);
+      const float tv = before ? val[j - 1] : val[j];
+      const int te = before ? se[j - 1] : se[j];
+      val[j - 1] = before ? val[j] : val[j - 1];
+      se[j - 1] = before ? se[j] : se[j - 1];
+      val[j] = tv;
+      se[j] = te;
     }
-  };
-  rescan();
+  }
+  // softmax denominator over every expert (renormalize off): before the
+  // rounds pop the winners out of the lists
+  const float row_max = warp_max_f32(val[0]);
+  float sacc = 0.f;
+  if (!v.renorm) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) sacc += expf(val[i] - row_max);  // -inf pads add 0
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  }
   int my_e = 0;
   float my_v = 0.f;
   for (int r = 0; r < k; ++r) {
-    const float bv = warp_max_f32(cv);
-    const int be = (int)__reduce_min_sync(0xffffffffu, cv == bv ? (unsigned)ce : 0xffffffffu);
+    const float bv = warp_max_f32(val[0]);
+    const int be = (int)__reduce_min_sync(0xffffffffu, val[0] == bv ? (unsigned)se[0] : 0xffffffffu);
     if (lane == r) { my_e = be; my_v = bv; }
-    if (be == ce) {  // this lane owned the winner
-      taken |= 1u << (4 * (be >> 7) + (be & 3));
-      rescan();
+    if (be == se[0]) {  // this lane owned the winner: pop its list head
+#pragma unroll
+      for (int i = 0; i + 1 < NV; ++i) {
+        val[i] = val[i + 1];
+        se[i] = se[i + 1];
+      }
+      val[NV - 1] = -INFINITY;
+      se[NV - 1] = 0x7fffffff;
     }
   }
-  const float mx = __shfl_sync(0xffffffffu, my_v, 0);  // top-1 = row max
-  const float ex = (lane < k) ? expf(my_v - mx) : 0.f;
+  const float ex = (lane < k) ? expf(my_v - row_max) : 0.f;
   float denom;
   if (v.renorm) {
     denom = ex;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
   } else {
-    float sacc = 0.f;
-#pragma unroll
-    for (int i = 0; i < EV * 4; ++i) {
-      const int e = 128 * (i >> 2) + 4 * lane + (i & 3);
-      if (e < E) sacc += expf(val[i] - mx);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
     denom = sacc;
   }
   if (lane < k) {
