@@ -287,25 +287,23 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
   __syncthreads();
 
   // ---- stable rank of each slot among the chunk's tokens of its expert,
-  //      and per-token host counts (token-major table order).
-  if (threadIdx.x < nt) {
-    const int tl = threadIdx.x;
-    for (int i = 0; i < k; ++i) {
-      const int e = s_ids[tl * k + i];
-      const int d = s_home[e];
-      int rk = 0;
-      for (int wd = 0; wd < (tl >> 5); ++wd) rk += __popc(s_mask[e * 4 + wd]);
-      rk += __popc(s_mask[e * 4 + (tl >> 5)] & ((1u << (tl & 31)) - 1u));
-      int within = 0;  // experts of this token on host d with a smaller id
-      for (int i2 = 0; i2 < k; ++i2) {
-        const int e2 = s_ids[tl * k + i2];
-        within += (e2 < e && s_home[e2] == d) ? 1 : 0;
-      }
-      const size_t si = (size_t)(t0 + tl) * k + i;
-      slot_rank[si] = rk;
-      slot_tmr[si] = within;
-      s_hc[tl * n + d] += 1;
+  //      and per-token host counts (token-major table order); thread per slot
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int tl = i / k, base = tl * k;
+    const int e = s_ids[i];
+    const int d = s_home[e];
+    int rk = 0;
+    for (int wd = 0; wd < (tl >> 5); ++wd) rk += __popc(s_mask[e * 4 + wd]);
+    rk += __popc(s_mask[e * 4 + (tl >> 5)] & ((1u << (tl & 31)) - 1u));
+    int within = 0;  // experts of this token on host d with a smaller id
+    for (int i2 = 0; i2 < k; ++i2) {
+      const int e2 = s_ids[base + i2];
+      within += (e2 < e && s_home[e2] == d) ? 1 : 0;
     }
+    const size_t si = (size_t)t0 * k + i;
+    slot_rank[si] = rk;
+    slot_tmr[si] = within;
+    atomicAdd(&s_hc[tl * n + d], 1);
   }
   __syncthreads();
   // exclusive scans over the chunk's tokens (4 per lane) of (a) the slot
