@@ -415,6 +415,14 @@ __global__ void __launch_bounds__(512) k_layout(DevView v) {
   const int* cnt = at<int>(v, v.rank, v.off.cnt_all);
   const int* ucnt = at<int>(v, v.rank, v.off.ucnt_all);
   const bool pub = blockIdx.x == 0;
+  // this thread's first slot, loaded under the table prologue below
+  const long long q_first = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int pf_e = 0, pf_r = 0, pf_m = 0;
+  if (q_first < (long long)v.T * k) {
+    pf_e = at<int>(v, v.rank, v.off.ids)[q_first];
+    pf_r = at<int>(v, v.rank, v.off.slot_rank)[q_first];
+    pf_m = at<int>(v, v.rank, v.off.slot_tmr)[q_first];
+  }
   for (int i = threadIdx.x; i < n * E; i += blockDim.x) s_cnt[i] = cnt[i];
   __syncthreads();
   // per-expert totals, own-group offsets, host-segmented exclusive scan
@@ -511,16 +519,17 @@ __global__ void __launch_bounds__(512) k_layout(DevView v) {
   int* slot_tm = at<int>(v, v.rank, v.off.slot_tm);
   int* err = at<int>(v, v.rank, v.off.err);
   const long long total = (long long)v.T * k;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
-       q += (long long)gridDim.x * blockDim.x) {
+  for (long long q = q_first; q < total; q += (long long)gridDim.x * blockDim.x) {
+    const bool first = q == q_first;
     const int t = (int)(q / k);
-    const int e = ids[q];
+    const int e = first ? pf_e : ids[q];
     const int d = home_of(e, n, E);
     const int c = t / MX_CHUNK;
-    const long long pos = (long long)s_exp_off[e] + s_grp_off[e] + chunk_hist[e * v.C + c] + slot_rank[q];
+    const long long pos = (long long)s_exp_off[e] + s_grp_off[e] + chunk_hist[e * v.C + c] +
+                          (first ? pf_r : slot_rank[q]);
     if (pos >= v.cap) atomicOr(err + 3, 1);
     slot_pos[q] = (int)pos;
-    slot_tm[q] = s_tm[d] + chunk_host[d * v.C + c] + slot_tmr[q];
+    slot_tm[q] = s_tm[d] + chunk_host[d * v.C + c] + (first ? pf_m : slot_tmr[q]);
   }
   const int* tpr = at<int>(v, v.rank, v.off.tok_pair_rank);
   const int* chunk_pair = at<int>(v, v.rank, v.off.chunk_pair);
