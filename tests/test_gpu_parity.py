@@ -603,6 +603,35 @@ def test_fp8_layer_vs_oracle(n, m, Is, wire):
     assert fro <= FP8_FRO and mx <= FP8_MAX, (fro, mx)
 
 
+@pytest.mark.parametrize("wire", ["token", "slot"])
+def test_config_b_full_size_8_ranks_emulated(wire):
+    """Config B at full size in the 8-GPU layout (TP2 x EP4, 8192 tokens,
+    128 experts top-8, h=2048, I=768), all 8 ranks emulated on one GPU:
+    the layer within the bf16 tolerance of the dense GPU oracle."""
+    from paper_2601_08800_b200 import SwiGLUExperts, moe_oracle, RouterSpec, _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    n, m, Tg, h, E, k, I = 4, 2, 8192, 2048, 128, 8, 768
+    ex = SwiGLUExperts.random(E, h, I, seed=31)
+    w13, w2 = ex.stacked_shards(n, m)
+    gen = torch.Generator(device="cuda").manual_seed(32)
+    x = torch.randn(Tg, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = torch.randn(Tg, E, device="cuda", generator=gen)
+    plan = LayerPlan(n, m, Tg // n, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu",
+                     inter=I, wire=wire)
+    y = torch.empty(Tg, h, dtype=torch.bfloat16, device="cuda")
+    plan.forward(x, N.ExpertParams(None, None, w13.data_ptr(), w2.data_ptr()), logits=logits,
+                 y_out=y)
+    ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    v = plan.rank_views(0)
+    assert np.array_equal(v["exp_cnt"].cpu().numpy(), np.bincount(ids.reshape(-1), minlength=E))
+    router = RouterSpec(E, tuple(map(tuple, ids.tolist())),
+                        tuple(map(tuple, w.astype(np.float64).tolist())))
+    y_d = moe_oracle(x, router, ex)
+    err = orc.verify_metric(y.float().cpu().numpy(), y_d.float().cpu().numpy())
+    assert err <= 2e-2, err
+    plan.close()
+
+
 def test_fp8_deepseek_shape_layer():
     """BASELINE configs[2] shape: h=7168, moe_intermediate=2048, top-8 with a
     2048-wide shared expert, TP4 x EP2 (emulated 8 ranks on one GPU); expert
