@@ -603,6 +603,39 @@ def test_fp8_layer_vs_oracle(n, m, Is, wire):
     assert fro <= FP8_FRO and mx <= FP8_MAX, (fro, mx)
 
 
+@pytest.mark.parametrize("n,m,wire,Is", [(2, 2, "token", 256), (2, 4, "slot", 512)])
+def test_fp8_layer_deepseek_gate(n, m, wire, Is):
+    """Config C end to end: DeepSeek-V3 group-limited gate (sigmoid, bias,
+    8 groups keep 4, routed scaling 2.5) feeding fp8 experts + shared expert;
+    ids bit-exact with the oracle router, layer within the fp8 tolerance."""
+    from paper_2601_08800_b200 import FP8SwiGLUExperts, _native as N
+    from paper_2601_08800_b200.plan import GateSpec, LayerPlan
+    T, h, E, k, I = 64, 512, 32, 4, 512
+    ex = FP8SwiGLUExperts.random(E, h, I, shared_inter=Is, seed=41)
+    gen = torch.Generator(device="cuda").manual_seed(42)
+    x = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = torch.randn(n * T, E, device="cuda", generator=gen)
+    bias = (0.05 * torch.randn(E, generator=torch.Generator().manual_seed(43))).float()
+    gate = GateSpec.deepseek_v3(bias, groups=8, topk_groups=4, scaling=2.5)
+    plan = LayerPlan(n, m, T, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu_fp8",
+                     inter=I, shared_inter=Is, wire=wire, gate=gate)
+    sh = ex.stacked_shards(n, m)
+    y = torch.empty(n * T, h, dtype=torch.bfloat16, device="cuda")
+    plan.forward(x, ex.params(sh), logits=logits, y_out=y)
+    ids, w = orc.router_group_limited(logits.cpu().numpy(), bias.numpy(), k, 8, 4, True, 2.5)
+    for r in range(n * m):
+        g = r // m
+        got = plan.rank_views(r)["ids"].cpu().numpy()
+        assert np.array_equal(got, ids[g * T:(g + 1) * T])
+    gate_w, up, down, shared = ex.oracle_arrays(n, m)
+    y_o = orc.moe_layer_fp8(x.float().cpu().numpy(), ids, w, gate_w, up, down, shared)
+    yg = y.double().cpu().numpy()
+    mx = orc.verify_metric(yg, y_o)
+    fro = float(np.linalg.norm(yg - y_o) / np.linalg.norm(y_o))
+    assert fro <= FP8_FRO and mx <= FP8_MAX, (fro, mx)
+    plan.close()
+
+
 @pytest.mark.parametrize("wire", ["token", "slot"])
 def test_config_b_full_size_8_ranks_emulated(wire):
     """Config B at full size in the 8-GPU layout (TP2 x EP4, 8192 tokens,

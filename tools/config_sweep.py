@@ -6,8 +6,8 @@ skew with strategy auto-selection) on the fused layer.
 
 C: h=7168, moe_intermediate=2048, 256 routed experts top-8 + a 2048-wide
    shared expert, fp8 e4m3 experts (per-channel weight scales, per-row
-   activation scales), 8192 tokens, every (TP, EP) layout of N GPUs with
-   TP >= 2.  Reports the fused forward (one CUDA graph) in tokens/s and
+   activation scales), the DeepSeek-V3 group-limited gate, 8192 tokens,
+   every (TP, EP) layout of N GPUs with TP >= 2.  Reports the fused forward (one CUDA graph) in tokens/s and
    the expert FLOP rate.
 E: the Qwen3-30B-A3B-shaped bf16 layer (config B) with gate logits
    N(0,1) + log p_e, p_e ∝ rank^-s (s in 0, 0.8, 1.0, 1.2), at every
@@ -31,6 +31,7 @@ import torch.distributed as dist
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2601_08800_b200 import FP8SwiGLUExperts, SwiGLUExperts  # noqa: E402
 from paper_2601_08800_b200.layer import MoELayer  # noqa: E402
+from paper_2601_08800_b200.plan import GateSpec  # noqa: E402
 from paper_2601_08800_b200.skew import host_skew, zipf_logits  # noqa: E402
 
 
@@ -70,10 +71,16 @@ def config_c(args, rank, world, flush):
         x = torch.randn(T, H, device="cuda", generator=gen).to(torch.bfloat16)
         logits = torch.randn(T, E, device="cuda", generator=gen)
         wire = "token" if world > 1 else "slot"
-        layer = MoELayer(n, m, T, H, E, K, I, ex, rank=rank, wire=wire)
+        # DeepSeek-V3 gate: sigmoid scores + correction bias, 8 groups keep 4,
+        # routed scaling 2.5 (transformers deepseek_v3 configuration)
+        bias = 0.05 * torch.randn(E, generator=torch.Generator().manual_seed(5))
+        layer = MoELayer(n, m, T, H, E, K, I, ex, rank=rank, wire=wire,
+                         gate=GateSpec.deepseek_v3(bias))
         run = layer.capture(x, logits)
         ms = timed(run, layer, args.iters, flush)
-        cnt = torch.bincount(torch.topk(logits, K, dim=1).indices.reshape(-1), minlength=E)
+        cnt = torch.bincount(layer.plan.rank_views(rank)["ids"].reshape(-1).long(), minlength=E)
+        if m > 1:  # TP ranks of a group route the same tokens: count each group once
+            cnt = cnt * (rank % m == 0)
         dist.all_reduce(cnt)
         slots = int(cnt.sum())
         # per-GPU expert flops (routed GEMM1+GEMM2 on the TP shard + shared expert)
@@ -82,6 +89,7 @@ def config_c(args, rank, world, flush):
         res = {"config": "C", "n_gpus": world, "layout": f"TP{m}xEP{n}", "wire": wire,
                "global_tokens": args.tokens, "hidden": H, "moe_intermediate": I, "experts": E,
                "top_k": K, "shared_inter": IS, "dtype": "fp8 e4m3 experts, bf16 tokens",
+               "gate": "DeepSeek-V3 group-limited (8 groups, top-4, scaling 2.5)",
                "ms_per_step": ms, "tokens_per_s": args.tokens / (ms / 1e3),
                "expert_tflops_per_gpu_incl_comm": flops / (ms / 1e3) / 1e12,
                "slots": slots}
