@@ -255,9 +255,24 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
         # each of the pair's slot rows
         model["expand"] = {"bound": "hbm", "bytes": remote_pairs * hb + remote_in * hb}
         pairs_host = int(U[:, group].sum())
-        model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * hb + pairs_host * hb}
-        pull = (int(U[group].sum()) * m - int(U[group, group])) * (H // m) * 2
-        model["combine"] = {"bound": "nvlink", "bytes": pull + T * H * (m - 1) // m * 2}
+        # the pre-reduction pushes each pair's row (as m column shards) into
+        # the owners' ZIN: all of it crosses NVLink for other groups' tokens,
+        # (m-1)/m of it for the own group's; it reads S_d partial rows locally
+        own = int(U[group, group])
+        push = (pairs_host - own) * hb + own * hb * (m - 1) // m
+        if push > 0:
+            model["pair_reduce"] = {"bound": "nvlink", "bytes": push,
+                                    "local_hbm_bytes": S_d * hb}
+        else:
+            model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * hb + pairs_host * hb}
+        # the owner sums its local ZIN planes and pushes its y shard to the
+        # group's other TP ranks (final all-gather)
+        zin_read = int(U[group].sum()) * hb
+        y_push = T * H * (m - 1) // m * 2
+        if y_push > 0:
+            model["combine"] = {"bound": "nvlink", "bytes": y_push, "local_hbm_bytes": zin_read}
+        else:
+            model["combine"] = {"bound": "hbm", "bytes": zin_read + T * hb}
     model["gemm1_swiglu"] = {"bound": "tensor", "flops": 2 * S_d * H * 2 * It}
     model["gemm2"] = {"bound": "tensor", "flops": 2 * S_d * It * H}
     return model

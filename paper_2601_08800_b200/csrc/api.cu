@@ -181,7 +181,8 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   o.pair_p = take(2 * wsz * U * KH);  // packed {row, weight} entries
   o.pair_w = take(0);
   o.pair_n = take(4 * U);
-  o.z = take(U * h * elt);
+  o.pair_tok = take(4 * U);
+  o.zin = take(tok ? (size_t)n * d.tp * T * ((h + d.tp - 1) / d.tp) * elt : 0);
   o.xq = take(fp8 ? T * wrow : 0);
   o.actq = take(fp8 ? (size_t)cap * (It + 16) : 0);
   o.act_s = take(T * Ist * 2);

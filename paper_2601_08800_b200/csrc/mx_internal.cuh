@@ -67,7 +67,9 @@ struct Offsets {
   size_t pair_p;      // int32 [T*n][KH] slot rows of a pair (peers write)
   size_t pair_w;      // AccT [T*n][KH]  slot weights of a pair (peers write)
   size_t pair_n;      // int32 [T*n]     slots of a pair (peers write)
-  size_t z;           // act [T*n][h]  pre-reduced w*partial per pair (peers read)
+  size_t pair_tok;    // int32 [T*n]     owner token (group*T + t) of a pair (peers write)
+  size_t zin;         // act [n][m][T][h/m] pre-reduced TP partials pushed by every
+                      //   host TP rank into the owner's shard (peers write)
   // fp8 experts (SWIGLU_FP8) and the shared expert
   size_t xq;          // [T][wrow]       this group's tokens, e4m3 + row scale
   size_t actq;        // [cap][I_t+16]   e4m3 activation + row scale (GEMM2 A)

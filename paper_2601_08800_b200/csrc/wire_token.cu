@@ -10,8 +10,9 @@
 //             XBUF; the host expands XBUF rows into its expert-major RECV
 //             (local HBM copy) before the grouped GEMM;
 //   combine:  each host TP rank pre-reduces z[u] = sum_i w_i * partial[p_i]
-//             over the token's slots on that host (experts ascending), and
-//             the owner pulls one z row shard per (host, TP rank).
+//             over the token's slots on that host (experts ascending) and
+//             pushes z's column shards straight into the owners' ZIN; the
+//             owner sums its local ZIN planes.
 // NVLink bytes per token drop from k rows to (#hosts hit) rows each way.
 #include "mx_internal.cuh"
 
@@ -159,7 +160,10 @@ __global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* _
       ent.p = p;
       ent.w = wts[t * k + lane];
       reinterpret_cast<PairEnt<WT>*>(at<char>(v, dst, v.off.pair_p))[(size_t)u * v.KH + idx] = ent;
-      if (idx == 0) at<int>(v, dst, v.off.pair_n)[u] = cnt;
+      if (idx == 0) {
+        at<int>(v, dst, v.off.pair_n)[u] = cnt;
+        at<int>(v, dst, v.off.pair_tok)[u] = v.group * v.T + (int)t;
+      }
     }
   }
   if (v.sync_signal) grid_signal(v);  // rows + pair lists landed: barrier #2
@@ -212,8 +216,26 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
   }
 }
 
-// z[u] = sum over the pair's slots (experts ascending) of w * partial[p];
-// all slot loads of a column vector are issued before use (KU in flight).
+// Destination of column c of pair-reduced row z (owner token tok = j*T + t)
+// in the owner's shard: TP rank tt of group j owns columns [c0, c1) and keeps
+// one [T][sw] plane per (host, host TP rank) in its ZIN.
+template <class T>
+__device__ __forceinline__ T* zin_dst(const DevView& v, int tok, int c, int sw) {
+  const int j = tok / v.T, t = tok - j * v.T;
+  int tt = 0, c0 = 0, c1 = 0;
+  for (; tt < v.m; ++tt) {
+    col_shard(v.h, v.m, tt, &c0, &c1);
+    if (c < c1) break;
+  }
+  return at<T>(v, j * v.m + tt, v.off.zin) +
+         (((size_t)v.group * v.m + v.tp_rank) * v.T + t) * sw + (c - c0);
+}
+
+// z = sum over the pair's slots (experts ascending) of w * partial[p], pushed
+// straight into the owners' shards over NVLink (the reduce-scatter of the
+// combine fused into the pre-reduction: the owner then only reads local
+// memory); all slot loads of a column vector are issued before use.
+
 template <int DT, class WT>
 __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
@@ -228,10 +250,11 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
   const T* part = at<T>(v, v.rank, v.off.partial);
-  T* z = at<T>(v, v.rank, v.off.z);
-  const int h = v.h;
+  const int* ptok = at<int>(v, v.rank, v.off.pair_tok);
+  const int h = v.h, sw = (h + v.m - 1) / v.m;
   for (long long u = gw; u < pairs; u += nwarps) {
     const int cnt = pn[u];
+    const int tok = ptok[u];
     const T* rp[KU];
     A w[KU];
 #pragma unroll
@@ -270,7 +293,7 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
           T out[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-          st_v4(z + (size_t)u * h + c + hh * 32 * V, *reinterpret_cast<uint4*>(out));
+          st_v4(zin_dst<T>(v, tok, c + hh * 32 * V, sw), *reinterpret_cast<uint4*>(out));
         }
       }
     }
@@ -288,18 +311,19 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
       T out[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-      st_v4(z + (size_t)u * h + c, *reinterpret_cast<uint4*>(out));
+      st_v4(zin_dst<T>(v, tok, c, sw), *reinterpret_cast<uint4*>(out));
     }
   }
-  if (v.sync_signal) grid_signal(v);  // z written: barrier #3
+  if (v.sync_signal) grid_signal(v);  // every owner's ZIN written: barrier #3
 }
 
-// Owner (j, t): y[tok, cols t] = sum over hosts (j-1, ..., j) and TP ranks
-// (ascending) of z; then push the shard to every TP rank of the group.
+// Owner (j, t): y[tok, cols t] = sum over host TP ranks (ascending) and hosts
+// (j-1, ..., j) of the pre-reduced partials the hosts pushed into this rank's
+// ZIN; then push the shard to every TP rank of the group (final all-gather).
 template <int DT>
 __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
-  if (v.sync_wait) grid_wait(v);  // every host's z is written
+  if (v.sync_wait) grid_wait(v);  // every host's pushes into ZIN have landed
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
@@ -311,23 +335,27 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
   const int* upos = at<int>(v, v.rank, v.off.upos);
   int c0, c1;
   col_shard(h, m, v.tp_rank, &c0, &c1);
+  // this rank's ZIN: one [T][sw] plane per (host, host TP rank), written by
+  // the hosts' pair pre-reductions -- local reads only
+  const int sw = (h + m - 1) / m;
+  const T* zin = at<T>(v, v.rank, v.off.zin) - c0;
   for (long long t = gw; t < v.T; t += nwarps) {
-    int hs[HMAX], us[HMAX], nh = 0;
+    int hs[HMAX], nh = 0;
     for (int i = 1; i <= n; ++i) {
       const int d = (j - i + n) % n;  // arrival order j-1, ..., j
       const int u = upos[t * n + d];
-      if (u >= 0 && nh < HMAX) { hs[nh] = d; us[nh] = u; ++nh; }
+      if (u >= 0 && nh < HMAX) hs[nh++] = d;
     }
     int c = c0 + lane * V;
     if (m * nh <= 4) {
-      // fast path: every (TP rank, host) z load of two column vectors is
-      // issued before any is consumed (<= 8 remote 16 B loads in flight per
-      // lane); the sum keeps the TP-rank-major, arrival-order association
+      // fast path: every (host TP rank, host) ZIN load of two column vectors
+      // is issued before any is consumed; the sum keeps the TP-rank-major,
+      // arrival-order association
       const T* src[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int tt = i / (nh > 0 ? nh : 1), a = i % (nh > 0 ? nh : 1);
-        src[i] = i < m * nh ? at<T>(v, hs[a] * m + tt, v.off.z) + (size_t)us[a] * h : nullptr;
+        src[i] = i < m * nh ? zin + (((size_t)hs[a] * m + tt) * v.T + t) * sw : nullptr;
       }
       for (; c + 32 * V < c1; c += 64 * V) {
         uint4 r0[4], r1[4];
@@ -384,7 +412,7 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
         uint4 raw[HMAX];
 #pragma unroll
         for (int a = 0; a < HMAX; ++a)
-          if (a < nh) raw[a] = ld_v4(at<T>(v, hs[a] * m + tt, v.off.z) + (size_t)us[a] * h + c);
+          if (a < nh) raw[a] = ld_v4(zin + (((size_t)hs[a] * m + tt) * v.T + t) * sw + c);
 #pragma unroll
         for (int a = 0; a < HMAX; ++a)
           if (a < nh) {
