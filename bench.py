@@ -36,6 +36,7 @@ sys.path.insert(0, str(ROOT))
 
 H, INTER, E, K_TOP, T_GLOBAL = 2048, 768, 128, 8, 8192
 NVLINK_PEER_GBS = 770.0      # measured peer copy, B200_PROFILING.md
+HBM_REF_GBS = 6539.5         # MEASURED_PEAKS.json copy bandwidth (bound selection only)
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -273,6 +274,16 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
             model["combine"] = {"bound": "nvlink", "bytes": y_push, "local_hbm_bytes": zin_read}
         else:
             model["combine"] = {"bound": "hbm", "bytes": zin_read + T * hb}
+    # a phase that moves both NVLink and local HBM bytes is judged against
+    # whichever of the two takes longer at its peak
+    for spec in model.values():
+        loc = spec.pop("local_hbm_bytes", None)
+        if loc is not None and spec["bound"] == "nvlink" and \
+                loc / HBM_REF_GBS > spec["bytes"] / NVLINK_PEER_GBS:
+            spec["nvlink_bytes"] = spec["bytes"]
+            spec["bound"], spec["bytes"] = "hbm", loc
+        elif loc is not None:
+            spec["local_hbm_bytes"] = loc
     model["gemm1_swiglu"] = {"bound": "tensor", "flops": 2 * S_d * H * 2 * It}
     model["gemm2"] = {"bound": "tensor", "flops": 2 * S_d * It * H}
     return model

@@ -6,7 +6,7 @@ all-to-all of the mean per-rank volume.  The fused B200 layer does neither:
 on one NVSwitch box it moves deduplicated (token, host) rows one hop, pre-
 reduces them per pair, and its TP sharding shrinks the grouped GEMMs' K and
 N -- which costs tensor-core efficiency the reference model cannot see.
-Measured at config B, 4 GPUs: EP4 0.331 ms vs TP2xEP2 0.366 ms on a uniform
+Measured at config B, 4 GPUs: EP4 0.319 ms vs TP2xEP2 0.341 ms on a uniform
 router, the reverse under Zipf skew (profiles/r01_configE_n4.jsonl), while
 the reference model ranks TP2xEP2 first at every skew.
 
@@ -47,7 +47,8 @@ class LayerCalibration:
     gemm_eff: dict = field(default_factory=lambda: {384: (0.67, 0.60), 768: (0.83, 0.73)})
     eff: dict = field(default_factory=lambda: {
         "dispatch_nvlink": 0.59, "dispatch_hbm": 0.86, "expand": 0.70,
-        "pair_reduce": 0.60, "combine_nvlink": 0.65, "combine_hbm": 0.63})
+        "pair_reduce": 0.60, "pair_push_nvlink": 0.49, "combine_nvlink": 0.40,
+        "combine_hbm": 0.63})
     route_layout_us: float = 32.0
     barrier_us: float = 6.0   # graph replay: ~5 us intrinsic (barrier_bench) + skew
 
@@ -118,10 +119,17 @@ def predict_layer(ids, n: int, m: int, num_experts: int, hidden: int, inter: int
             disp = max(remote_pairs * hb / (c.eff["dispatch_nvlink"] * nvl),
                        (T + local) * hb / (c.eff["dispatch_hbm"] * hbm))
             exp_ = (remote_pairs + remote_in) * hb / (c.eff["expand"] * hbm)
-            pr = (S_d + pairs) * hb / (c.eff["pair_reduce"] * hbm)
-            pull = (int(U[d].sum()) * m - int(U[d, d])) * (hidden // m) * elt
-            push = T * hidden * (m - 1) // m * elt
-            comb = (pull + push) / (c.eff["combine_nvlink"] * nvl)
+            # pre-reduction: reads the host's slot partials, pushes each pair
+            # row's shards into the owners (NVLink except the own shard)
+            own = int(U[d, d])
+            push = (pairs - own) * hb + own * hb * (m - 1) // m
+            pr = max(S_d * hb / (c.eff["pair_reduce"] * hbm),
+                     push / (c.eff["pair_push_nvlink"] * nvl))
+            # owner: local ZIN planes, y shard pushed to the TP peers
+            zin = int(U[d].sum()) * hb
+            ypush = T * hidden * (m - 1) // m * elt
+            comb = max(zin / (c.eff["combine_hbm"] * hbm),
+                       ypush / (c.eff["combine_nvlink"] * nvl))
             pre, expert = disp, exp_ + g1 + g2 + pr
         seg["pre"] = max(seg["pre"], pre)
         seg["expert"] = max(seg["expert"], expert)

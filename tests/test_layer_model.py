@@ -41,13 +41,14 @@ def test_layouts_respect_the_tp_shard_rule():
 @pytest.mark.parametrize("s,best", [(0.0, "TP1xEP4"), (0.8, "TP2xEP2"), (1.0, "TP2xEP2"),
                                     (1.2, "TP2xEP2")])
 def test_ranking_matches_measured_config_e(s, best):
-    """Measured at 4 x B200 (round 1): EP4 0.330 ms vs TP2xEP2 0.366 ms at
-    s=0; TP2xEP2 0.384-0.388 ms vs EP4 0.403-0.424 ms for s >= 0.8."""
+    """Measured at 4 x B200 (round 1, profiles/r01_configE_n4.jsonl): EP4
+    0.319 ms vs TP2xEP2 0.341 ms at s=0; TP2xEP2 0.348-0.351 ms vs EP4
+    0.375-0.395 ms for s >= 0.8."""
     assert select_layout(_ids(s), 4, E, H, I)[0]["layout"] == best
 
 
-@pytest.mark.parametrize("n,m,measured_ms", [(1, 1, 0.702), (2, 1, 0.457), (2, 2, 0.366),
-                                             (4, 1, 0.331)])
+@pytest.mark.parametrize("n,m,measured_ms", [(1, 1, 0.688), (2, 1, 0.446), (2, 2, 0.344),
+                                             (4, 1, 0.317)])
 def test_predictions_near_measured(n, m, measured_ms):
     # measured: bench.py lines of profiles/r01_n{1,2,4}_bench.json
     # (value and layout_ep_only), uniform router
