@@ -192,8 +192,10 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
     skip0 = at<int>(v, v.rank, v.off.poff)[g * v.n + g];
     skip1 = skip0 + at<int>(v, v.rank, v.off.ucnt_all)[g * v.n + g];
   }
-  for (long long u = gw; u < pairs; u += nwarps) {
-    if (u >= skip0 && u < skip1) continue;
+  // warps walk only the pairs left to expand (the own-group block skipped)
+  const long long todo = pairs - (skip1 - skip0);
+  for (long long r = gw; r < todo; r += nwarps) {
+    const long long u = r < skip0 ? r : r + (skip1 - skip0);
     const int cnt = pn[u];
     int rows[MX_KMAX];
     for (int i = 0; i < cnt; ++i) rows[i] = pe[u * v.KH + i].p;
