@@ -142,6 +142,8 @@ class RouterSpec:
         if len(ks) > 1:
             raise StrategyError("the B200 router needs the same top-k for every token")
         k = ks.pop() if ks else 0
+        if not self.expert_ids:  # empty batch
+            return np.zeros((0, 0), dtype=np.int32), np.zeros((0, 0), dtype=np.float64)
         ids = np.asarray(self.expert_ids, dtype=np.int32).reshape(-1, k)
         w = np.asarray(self.weights, dtype=np.float64).reshape(-1, k)
         return ids, w
@@ -737,6 +739,17 @@ def run_moe_block(cluster: SimCluster, x_global, router: RouterSpec, experts,
         dtype = torch.float64 if numpy_in else x_global.dtype
     xg = _to_dev(x_global, dtype).contiguous()
     ids, _ = router.arrays()
+    if T == 0:
+        # empty batch: nothing to route or move; the reference still emits
+        # its zero-byte event schedule (sim:353-520), and so does the builder
+        tb = TraceBuilder(n, m, 0, h, np.zeros((n, n), dtype=np.int64))
+        if mode == "fused":
+            tb.dispatch()
+            tb.combine(tb.expert([[] for _ in range(n)], tb.expert_deps()))
+        else:
+            tb.baseline([[] for _ in range(n)])
+        y = torch.empty(0, h, dtype=dtype, device=xg.device)
+        return (y.double().cpu().numpy() if numpy_in else y), tb.trace
     plan = _plan(n, m, T, h, router.num_experts, ids.shape[1], dtype, kind,
                  experts.I if kind != "affine" else 0, capacity,
                  experts.Is if kind == "swiglu_fp8" else 0)

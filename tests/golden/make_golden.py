@@ -70,6 +70,11 @@ def main():
                 x=np.arange(32.0).reshape(4, 8))
     (HERE / "trace_2x2.csv").write_text(
         str(np.load(HERE / "ref_2x2_golden.npz")["trace_csv"]))
+    # empty batch: the reference still emits its zero-byte event schedule
+    for mode in ("fused", "baseline"):
+        _, tr = run_moe_block(build_cluster(2, 2), np.zeros((0, 8)), RouterSpec(4, (), ()),
+                              ExpertSpec.default(4), mode=mode)
+        (HERE / f"trace_empty_2x2_{mode}.csv").write_text(trace_to_csv(tr.events))
     # BASELINE.json configs[0]: n=2, m=2, 256 tokens, h=512, 8 experts top-2
     routed_case("ref_config_a", 2, 2, 256, 2, 8, 512, 1)
     # shape grid after pkg/tests/test_simcluster.py:216-224 and

@@ -139,6 +139,58 @@ def test_rs_combine_from_oracle_partials():
     assert np.array_equal(np.concatenate(ys), g["y_fused"])
 
 
+@pytest.mark.parametrize("mode", ["fused", "baseline"])
+def test_empty_batch_matches_reference(mode):
+    """Zero tokens: the reference returns an empty output and its zero-byte
+    event schedule; same shape, byte-identical trace (frozen by
+    tests/golden/make_golden.py)."""
+    from conftest import GOLDEN
+    from paper_2601_08800_b200 import ExpertSpec, RouterSpec, build_cluster, run_moe_block
+    from paper_2601_08800_b200.trace import trace_to_csv
+    x = np.zeros((0, 8))
+    y, tr = run_moe_block(build_cluster(2, 2), x, RouterSpec(4, (), ()), ExpertSpec.default(4),
+                          mode=mode)
+    assert y.shape == (0, 8)
+    assert trace_to_csv(tr.events) == (GOLDEN / f"trace_empty_2x2_{mode}.csv").read_text()
+
+
+def test_verify_detects_corrupted_output():
+    """verify_against_oracle raises VerificationError on a perturbed output
+    (T/test_simcluster.py: corrupted output detected)."""
+    from paper_2601_08800_b200 import (ExpertSpec, RouterSpec, VerificationError,
+                                       build_cluster, run_moe_block, verify_against_oracle)
+    x = np.arange(32.0).reshape(4, 8)
+    router = RouterSpec.round_robin(4, 2, 1)
+    y, _ = run_moe_block(build_cluster(2, 2), x, router, ExpertSpec.default(2))
+    assert verify_against_oracle(y, x, router, ExpertSpec.default(2)) == 0.0
+    y2 = y.copy()
+    y2[0, 0] += 1.0
+    with pytest.raises(VerificationError):
+        verify_against_oracle(y2, x, router, ExpertSpec.default(2))
+
+
+def test_randomized_shapes_f64_bit_exact():
+    """Seeded random clusters and shapes (the reference's hypothesis
+    equivalence test, T/test_simcluster.py:216-252): the fused f64 layer is
+    bit-identical to the oracle's restatement of the reference value path."""
+    from paper_2601_08800_b200 import ExpertSpec, RouterSpec, build_cluster, run_moe_block
+    rng = np.random.default_rng(2026)
+    for _ in range(12):
+        n, m = int(rng.integers(1, 5)), int(rng.integers(1, 4))
+        E = int(rng.integers(n, 3 * n + 6))
+        k = int(rng.integers(1, min(E, 6) + 1))
+        T = int(rng.integers(1, 40))
+        h = int(rng.integers(m, 48))
+        x = rng.standard_normal((n * T, h))
+        router = RouterSpec.random(n * T, E, k, seed=int(rng.integers(1 << 30)))
+        experts = ExpertSpec(tuple(rng.standard_normal(E).tolist()),
+                             tuple(rng.standard_normal(E).tolist()))
+        y, _ = run_moe_block(build_cluster(n, m), x, router, experts)
+        ids, w = router.arrays()
+        y_ref, _ = orc.run_fused_affine(n, m, x, ids, w, E, experts.scales, experts.biases)
+        assert np.array_equal(y, y_ref), (n, m, E, k, T, h)
+
+
 def test_capacity_error():
     from paper_2601_08800_b200 import (CapacityError, RouterSpec, build_cluster,
                                        fused_ag_dispatch)
