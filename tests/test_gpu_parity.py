@@ -169,6 +169,34 @@ def test_verify_detects_corrupted_output():
         verify_against_oracle(y2, x, router, ExpertSpec.default(2))
 
 
+def test_expert_permutation_safety_and_determinism():
+    """Relabelling the experts consistently in router and experts leaves the
+    layer output unchanged (T/test_simcluster.py:232-251, rtol 1e-9); two
+    runs are byte-identical, trace included (:225-229)."""
+    from paper_2601_08800_b200 import ExpertSpec, RouterSpec, build_cluster, run_moe_block
+    from paper_2601_08800_b200.trace import trace_to_csv
+    rng = np.random.default_rng(17)
+    n, m, T, k, E = 2, 2, 8, 2, 4
+    x = rng.standard_normal((n * T, 16))
+    router = RouterSpec.random(n * T, E, k, seed=17)
+    experts = ExpertSpec(tuple(rng.standard_normal(E).tolist()), tuple(rng.standard_normal(E).tolist()))
+    perm = [2, 0, 3, 1]
+    prouter = RouterSpec(
+        E, tuple(tuple(sorted(perm[e] for e in ids)) for ids in router.expert_ids),
+        tuple(tuple(w for _, w in sorted((perm[e], w) for e, w in zip(ids, ws)))
+              for ids, ws in zip(router.expert_ids, router.weights)))
+    inv = [perm.index(e) for e in range(E)]
+    pexperts = ExpertSpec(tuple(experts.scales[inv[e]] for e in range(E)),
+                          tuple(experts.biases[inv[e]] for e in range(E)))
+    cl = build_cluster(n, m)
+    y1, t1 = run_moe_block(cl, x, router, experts)
+    y1b, t1b = run_moe_block(cl, x, router, experts)
+    y2, _ = run_moe_block(cl, x, prouter, pexperts)
+    assert np.array_equal(y1, y1b)
+    assert trace_to_csv(t1.events) == trace_to_csv(t1b.events)
+    assert np.allclose(y1, y2, rtol=1e-9, atol=1e-12)
+
+
 def test_randomized_shapes_f64_bit_exact():
     """Seeded random clusters and shapes (the reference's hypothesis
     equivalence test, T/test_simcluster.py:216-252): the fused f64 layer is
