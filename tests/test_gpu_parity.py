@@ -219,6 +219,18 @@ def test_randomized_shapes_f64_bit_exact():
         assert np.array_equal(y, y_ref), (n, m, E, k, T, h)
 
 
+def test_partial_shape_mismatch_raises():
+    """fused_rs_combine rejects partials of the wrong shape (sim:421-429;
+    T/test_simcluster.py:200-206)."""
+    from paper_2601_08800_b200 import (RouterSpec, StrategyError, build_cluster,
+                                       build_routing_table, fused_rs_combine)
+    cluster = build_cluster(2, 2)
+    table = build_routing_table(RouterSpec.round_robin(4, 4, 1), 2, 2)
+    bad = [[np.zeros((1, 8)), np.zeros((1, 8))] for _ in range(2)]
+    with pytest.raises(StrategyError, match="mismatch"):
+        fused_rs_combine(cluster, bad, table)
+
+
 def test_capacity_error():
     from paper_2601_08800_b200 import (CapacityError, RouterSpec, build_cluster,
                                        fused_ag_dispatch)

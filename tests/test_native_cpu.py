@@ -80,3 +80,22 @@ def test_trace_csv_round_trip_and_bad_line():
            "0,0,route,local,oops,0,,compute,1,0.0\n")
     with pytest.raises(ValueError, match="line 2"):
         trace_from_csv(bad)
+
+
+def test_router_validation_matches_reference():
+    """RouterSpec rejects duplicate and out-of-range ids like the reference
+    (sim:153-162; T/test_simcluster.py:93-98)."""
+    from paper_2601_08800_b200 import RouterSpec
+    with pytest.raises(ValueError, match="duplicate"):
+        RouterSpec(4, ((0, 0),), ((0.5, 0.5),))
+    with pytest.raises(ValueError, match="out of range"):
+        RouterSpec(2, ((0, 2),), ((0.5, 0.5),))
+
+
+def test_malformed_trace_row_names_its_line():
+    """trace_from_csv names the offending line (T/test_simcluster.py:264-268)."""
+    from paper_2601_08800_b200.trace import trace_from_csv
+    text = ("event_id,rank,op,peer_or_group,bytes,round,dep_ids,scope,group_size,work\n"
+            "0,0,route,local,oops,0,,compute,1,0.0\n")
+    with pytest.raises(ValueError, match="line 2"):
+        trace_from_csv(text)
