@@ -46,7 +46,7 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 // own group) once per host it hits, then publish per-slot metadata to the TP
 // peer on that host: the pair's packed (slot row, weight) list and its length.
 template <class WT>
-__global__ void __launch_bounds__(256) k_dispatch_token(DevView v, const char* __restrict__ x) {
+__global__ void __launch_bounds__(256, 3) k_dispatch_token(DevView v, const char* __restrict__ x) {
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   // DSPLIT warps per token, each moving its slice of the row's 16 B vectors
@@ -220,31 +220,92 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
 
 // Destination of column c of pair-reduced row z (owner token tok = j*T + t)
 // in the owner's shard: TP rank tt of group j owns columns [c0, c1) and keeps
-// one [T][sw] plane per (host, host TP rank) in its ZIN.
+// one [T][sw] plane per (host, host TP rank) in its ZIN.  A lane's columns
+// only grow along a row, so the cursor advances the shard incrementally
+// (no division or shard search per store).
 template <class T>
-__device__ __forceinline__ T* zin_dst(const DevView& v, int tok, int c, int sw) {
-  const int j = tok / v.T, t = tok - j * v.T;
-  int tt = 0, c0 = 0, c1 = 0;
-  for (; tt < v.m; ++tt) {
-    col_shard(v.h, v.m, tt, &c0, &c1);
-    if (c < c1) break;
+struct ZinCursor {
+  int j, tt, c0, c1;
+  size_t rowoff;
+  T* base;
+  __device__ __forceinline__ ZinCursor(const DevView& v, int tok, int sw) {
+    j = tok / v.T;
+    const int t = tok - j * v.T;
+    rowoff = (((size_t)v.group * v.m + v.tp_rank) * v.T + t) * sw;
+    tt = 0;
+    col_shard(v.h, v.m, 0, &c0, &c1);
+    base = at<T>(v, j * v.m, v.off.zin) + rowoff;
   }
-  return at<T>(v, j * v.m + tt, v.off.zin) +
-         (((size_t)v.group * v.m + v.tp_rank) * v.T + t) * sw + (c - c0);
-}
+  __device__ __forceinline__ T* operator()(const DevView& v, int c) {
+    while (c >= c1 && tt + 1 < v.m) {
+      ++tt;
+      col_shard(v.h, v.m, tt, &c0, &c1);
+      base = at<T>(v, j * v.m + tt, v.off.zin) + rowoff;
+    }
+    return base + (c - c0);
+  }
+};
 
 // z = sum over the pair's slots (experts ascending) of w * partial[p], pushed
 // straight into the owners' shards over NVLink (the reduce-scatter of the
 // combine fused into the pre-reduction: the owner then only reads local
 // memory); all slot loads of a column vector are issued before use.
 
+template <int DT, class WT, int CV, int KR>
+__device__ __forceinline__ void pair_rows(const DevView& v, const typename Elt<DT>::T* part,
+                                          const int* prow, const typename Elt<DT>::Acc* w,
+                                          int cnt, int tok, int lane) {
+  // CV column vectors per lane per round, all cnt (<= KR) slot loads of a
+  // round issued before use
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  constexpr int V = Elt<DT>::V;
+  const int h = v.h, sw = (h + v.m - 1) / v.m;
+  ZinCursor<T> zc(v, tok, sw);
+  for (int c = lane * V; c < h; c += CV * 32 * V) {
+    uint4 raw[CV][KR];
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+      if (i < cnt)
+#pragma unroll
+        for (int cv = 0; cv < CV; ++cv)
+          if (c + cv * 32 * V < h)
+            raw[cv][i] = ld_v4(part + (size_t)prow[i] * h + c + cv * 32 * V);
+#pragma unroll
+    for (int cv = 0; cv < CV; ++cv) {
+      if (c + cv * 32 * V >= h) break;
+      A acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = (A)0;
+#pragma unroll
+      for (int i = 0; i < KR; ++i)
+        if (i < cnt) {
+          const T* pv = reinterpret_cast<const T*>(&raw[cv][i]);
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            if constexpr (DT == MX_F64)  // reference association, uncontracted
+              acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+            else
+              acc[q] = fmaf(w[i], to_acc(pv[q]), acc[q]);
+          }
+        }
+      T out[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+      st_v4(zc(v, c + cv * 32 * V), *reinterpret_cast<uint4*>(out));
+    }
+  }
+}
+
+// Persistent warps walk the host's pairs; the next pair's count, owner and
+// slot entries (lane i holds entry i) are loaded while the current pair's
+// rows are reduced, so only the row loads sit on each pair's critical path.
 template <int DT, class WT>
-__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
+__global__ void __launch_bounds__(256, 1) k_pair_reduce(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
-  constexpr int KU = 8;
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -254,66 +315,243 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
   const T* part = at<T>(v, v.rank, v.off.partial);
   const int* ptok = at<int>(v, v.rank, v.off.pair_tok);
   const int h = v.h, sw = (h + v.m - 1) / v.m;
+  int cnt = 0, tok = 0;
+  PairEnt<WT> ent{};
+  if (gw < pairs) {
+    cnt = pn[gw];
+    tok = ptok[gw];
+    if (lane < v.KH) ent = pe[gw * v.KH + lane];
+  }
   for (long long u = gw; u < pairs; u += nwarps) {
-    const int cnt = pn[u];
-    const int tok = ptok[u];
-    const T* rp[KU];
-    A w[KU];
-#pragma unroll
-    for (int i = 0; i < KU; ++i) {
-      const PairEnt<WT> e = pe[u * v.KH + (i < cnt ? i : 0)];
-      rp[i] = part + (size_t)e.p * h;
-      w[i] = (A)e.w;
+    const long long un = u + nwarps;
+    int ncnt = 0, ntok = 0;
+    PairEnt<WT> nent{};
+    if (un < pairs) {
+      ncnt = pn[un];
+      ntok = ptok[un];
+      if (lane < v.KH) nent = pe[un * v.KH + lane];
     }
-    int c = lane * V;
-    if (cnt <= KU) {
-      for (; c + 32 * V < h; c += 64 * V) {  // two column vectors per lane: 2 x cnt loads in flight
-        uint4 raw[2][KU];
+    if (cnt <= 8) {
+      int prow[8];
+      A w[8];
 #pragma unroll
-        for (int i = 0; i < KU; ++i)
-          if (i < cnt) {
-            raw[0][i] = ld_v4(rp[i] + c);
-            raw[1][i] = ld_v4(rp[i] + c + 32 * V);
-          }
+      for (int i = 0; i < 8; ++i) {
+        const int src = i < cnt ? i : 0;
+        prow[i] = __shfl_sync(0xffffffffu, ent.p, src);
+        w[i] = (A)__shfl_sync(0xffffffffu, ent.w, src);
+      }
+      if (cnt <= 4) pair_rows<DT, WT, 4, 4>(v, part, prow, w, cnt, tok, lane);
+      else pair_rows<DT, WT, 2, 8>(v, part, prow, w, cnt, tok, lane);
+    } else {
+      ZinCursor<T> zc(v, tok, sw);
+      for (int c = lane * V; c < h; c += 32 * V) {
+        A acc[V];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        for (int q = 0; q < V; ++q) acc[q] = (A)0;
+        for (int i = 0; i < cnt; ++i) {
+          const PairEnt<WT> e = pe[u * v.KH + i];
+          const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+          const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
+        }
+        T out[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+        st_v4(zc(v, c), *reinterpret_cast<uint4*>(out));
+      }
+    }
+    cnt = ncnt;
+    tok = ntok;
+    ent = nent;
+  }
+  if (v.sync_signal) grid_signal(v);  // every owner's ZIN written: barrier #3
+}
+
+// Bulk-copy pre-reduction (bf16 / f32 rows, at most 8 slots per pair read
+// from shared memory; larger pairs straight from HBM).  The register kernel
+// above keeps only as many slot rows in flight as its registers hold -- one
+// CTA per SM, 12% warps active, 51 us for one config-B rank's 134 MB on the
+// emulated cluster (tools/emu_layer.py under ncu).  Here the TMA engine
+// streams the rows into a ring of row slots in shared memory and registers
+// only hold the sums (43-45 us emulated; 59.8 vs 62.6-66 us inside the 4-GPU
+// layer, where the NVLink pushes bound it):
+//   warp 0      producer: walks the CTA's contiguous range of pairs, four at
+//               a time (lane l: entry l&7 of pair l>>3, two batches ahead),
+//               writes each pair's header (count, owner token, first slot,
+//               weights) and issues one cp.async.bulk per slot row,
+//               completing on the slot's full barrier;
+//   warps 1..15 consumers: pair i goes to warp 1 + i%15, which sums its rows
+//               from shared memory (experts ascending, as above), pushes the
+//               result into the owners' ZIN and frees the slots.  A single
+//               consumer is issue-latency bound (ncu: 5.8 cycles per issued
+//               instruction), hence many consumers and the ZinCursor.
+constexpr int PRB_WARPS = 16, PRB_NC = PRB_WARPS - 1, PRB_NP = 32, PRB_KU = 8;
+struct PrbHdr {
+  int cnt, tok;
+  unsigned q0;
+  int u;
+  float w[PRB_KU];
+};
+
+__host__ __device__ inline int prb_slots(size_t row_bytes) {
+  const long long n = (200LL * 1024) / (long long)row_bytes;
+  return (int)(n > 64 ? 64 : n);
+}
+__host__ __device__ inline size_t prb_smem(size_t row_bytes) {
+  const int ns = prb_slots(row_bytes);
+  return 128 + (size_t)ns * row_bytes + (2 * ns + 2 * PRB_NP) * 8 + PRB_NP * sizeof(PrbHdr);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView v) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  using T = typename Elt<DT>::T;
+  using A = typename Elt<DT>::Acc;
+  constexpr int V = Elt<DT>::V;
+  extern __shared__ __align__(128) unsigned char prb_raw[];
+  const int h = v.h, sw = (h + v.m - 1) / v.m;
+  const uint32_t row_bytes = (uint32_t)h * sizeof(T);
+  const int NS = prb_slots(row_bytes);
+  unsigned char* slots = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(prb_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + (size_t)NS * row_bytes);
+  uint64_t* empty = full + NS;
+  uint64_t* pfull = empty + NS;
+  uint64_t* pempty = pfull + PRB_NP;
+  PrbHdr* hdr = reinterpret_cast<PrbHdr*>(pempty + PRB_NP);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < PRB_NP; ++i) {
+      mbar_init(&pfull[i], 1);
+      mbar_init(&pempty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
+  const long long u0 = (long long)pairs * blockIdx.x / gridDim.x;
+  const long long u1 = (long long)pairs * (blockIdx.x + 1) / gridDim.x;
+  const int* pn = at<int>(v, v.rank, v.off.pair_n);
+  const PairEnt<float>* pe = reinterpret_cast<const PairEnt<float>*>(at<char>(v, v.rank, v.off.pair_p));
+  const T* part = at<T>(v, v.rank, v.off.partial);
+  if (warp == 0) {
+    const int* ptok = at<int>(v, v.rank, v.off.pair_tok);
+    unsigned q = 0;
+    // metadata of batch b (4 pairs; lane l: pair l>>3, entry l&7), loaded
+    // two batches ahead of its bulk copies
+    struct Meta {
+      int cnt, tok;
+      PairEnt<float> e;
+    };
+    auto load_meta = [&](long long b) {
+      Meta mt{0, 0, {}};
+      const long long ub = b + (lane >> 3);
+      const int j = lane & 7;
+      if (ub < u1) {
+        mt.cnt = pn[ub];
+        mt.tok = ptok[ub];
+        if (j < v.KH) mt.e = pe[ub * v.KH + j];
+      }
+      return mt;
+    };
+    Meta m0 = load_meta(u0), m1 = load_meta(u0 + 4);
+    for (long long b = u0; b < u1; b += 4) {
+      const Meta m2 = load_meta(b + 8);
+      const int j = lane & 7;
+      const int cnt_l = m0.cnt, tok_l = m0.tok;
+      const PairEnt<float> e = m0.e;
+      for (int pb = 0; pb < 4; ++pb) {
+        if (b + pb >= u1) break;
+        const int cnt = __shfl_sync(0xffffffffu, cnt_l, pb * 8);
+        const int tok = __shfl_sync(0xffffffffu, tok_l, pb * 8);
+        const int ep = __shfl_sync(0xffffffffu, e.p, pb * 8 + j);
+        const float ew = __shfl_sync(0xffffffffu, e.w, pb * 8 + j);
+        const long long i = b + pb - u0;
+        const int pi = (int)(i % PRB_NP);
+        mbar_wait(&pempty[pi], (uint32_t)((i / PRB_NP) & 1) ^ 1u);
+        const bool staged = cnt <= PRB_KU;
+        if (staged && lane < cnt) {
+          const unsigned qs = q + lane;
+          const int sl = (int)(qs % NS);
+          mbar_wait(&empty[sl], ((qs / NS) & 1) ^ 1u);
+          mbar_expect_tx(&full[sl], row_bytes);
+          bulk_load(slots + (size_t)sl * row_bytes, part + (size_t)ep * h, row_bytes, &full[sl]);
+        }
+        if (lane < PRB_KU) hdr[pi].w[lane] = ew;
+        if (lane == 0) {
+          hdr[pi].cnt = cnt;
+          hdr[pi].tok = tok;
+          hdr[pi].q0 = q;
+          hdr[pi].u = (int)(b + pb);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[pi]);
+        if (staged) q += cnt;
+      }
+      m0 = m1;
+      m1 = m2;
+    }
+  } else {
+    for (long long i = warp - 1; i < u1 - u0; i += PRB_NC) {
+      const int pi = (int)(i % PRB_NP);
+      mbar_wait(&pfull[pi], (uint32_t)((i / PRB_NP) & 1));
+      const int cnt = hdr[pi].cnt, tok = hdr[pi].tok, u = hdr[pi].u;
+      const unsigned q0 = hdr[pi].q0;
+      A w[PRB_KU];
+#pragma unroll
+      for (int jj = 0; jj < PRB_KU; ++jj) w[jj] = (A)hdr[pi].w[jj];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pempty[pi]);
+      ZinCursor<T> zc(v, tok, sw);
+      if (cnt <= PRB_KU) {
+        for (int jj = 0; jj < cnt; ++jj) {
+          const unsigned qs = q0 + jj;
+          mbar_wait(&full[qs % NS], (qs / NS) & 1);
+        }
+        for (int c = lane * V; c < h; c += 32 * V) {
           A acc[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) acc[q] = (A)0;
 #pragma unroll
-          for (int i = 0; i < KU; ++i)
-            if (i < cnt) {
-              const T* pv = reinterpret_cast<const T*>(&raw[hh][i]);
+          for (int jj = 0; jj < PRB_KU; ++jj)
+            if (jj < cnt) {
+              const unsigned qs = q0 + jj;
+              const uint4 raw = *reinterpret_cast<const uint4*>(
+                  slots + (size_t)(qs % NS) * row_bytes + (size_t)c * sizeof(T));
+              const T* pv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-              for (int q = 0; q < V; ++q) {
-                if constexpr (DT == MX_F64)  // reference association, uncontracted
-                  acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
-                else
-                  acc[q] = fmaf(w[i], to_acc(pv[q]), acc[q]);
-              }
+              for (int q = 0; q < V; ++q) acc[q] = fmaf(w[jj], to_acc(pv[q]), acc[q]);
             }
           T out[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-          st_v4(zin_dst<T>(v, tok, c + hh * 32 * V, sw), *reinterpret_cast<uint4*>(out));
+          st_v4(zc(v, c), *reinterpret_cast<uint4*>(out));
+        }
+        __syncwarp();
+        if (lane < cnt) mbar_arrive(&empty[(q0 + lane) % NS]);
+      } else {  // more slots than the staging handles: straight from HBM
+        for (int c = lane * V; c < h; c += 32 * V) {
+          A acc[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = (A)0;
+          for (int jj = 0; jj < cnt; ++jj) {
+            const PairEnt<float> e = pe[(long long)u * v.KH + jj];
+            const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+            const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
+          }
+          T out[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+          st_v4(zc(v, c), *reinterpret_cast<uint4*>(out));
         }
       }
-    }
-    for (; c < h; c += 32 * V) {
-      A acc[V];
-#pragma unroll
-      for (int q = 0; q < V; ++q) acc[q] = (A)0;
-      for (int i = 0; i < cnt; ++i) {
-        const PairEnt<WT> e = pe[u * v.KH + i];
-        const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
-        const T* pv = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
-      }
-      T out[V];
-#pragma unroll
-      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-      st_v4(zin_dst<T>(v, tok, c, sw), *reinterpret_cast<uint4*>(out));
     }
   }
   if (v.sync_signal) grid_signal(v);  // every owner's ZIN written: barrier #3
@@ -506,7 +744,24 @@ int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
 }
 
 int launch_pair_reduce(const DevView& v, cudaStream_t s) {
-  const int g = blocks_for((long long)v.T * v.n);
+  const size_t row_bytes = (size_t)v.h * v.elt;
+  if (v.elt != 8 && v.T > 0 && prb_slots(row_bytes) >= PRB_KU) {
+    auto kern = v.elt == 4 ? k_pair_reduce_bulk<MX_F32> : k_pair_reduce_bulk<MX_BF16>;
+    static bool attr[2] = {false, false};
+    if (!attr[v.elt == 4]) {
+      MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr[v.elt == 4] = true;
+    }
+    long long g = ((long long)v.T * v.n + 31) / 32;  // >= 32 pairs per CTA
+    if (g > 148) g = 148;
+    if (g < 1) g = 1;
+    pdl_launch(kern, (int)g, PRB_WARPS * 32, prb_smem(row_bytes), s, v);
+    MX_LAUNCH_CHECK();
+    return MX_OK;
+  }
+  // f64 (reference association) and rows too wide to stage: register kernel
+  int g = blocks_for((long long)v.T * v.n);
+  if (g > 148) g = 148;  // persistent, one CTA per SM
   switch (v.elt) {
     case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, 256, 0, s, v); break;
     case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, 256, 0, s, v); break;

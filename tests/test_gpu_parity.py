@@ -565,6 +565,59 @@ def test_wire_token_swiglu_emulated(shape):
     plan.close()
 
 
+@pytest.mark.parametrize("shape,k", [((2, 2), 12), ((1, 2), 12), ((4, 1), 6)])
+def test_wire_token_pair_reduce_slot_counts(shape, k):
+    """The bulk-copy pre-reduction stages pairs of at most 8 slots in shared
+    memory and reads larger pairs straight from HBM: top-k 12 mixes both
+    (all pairs exceed 8 slots on one host)."""
+    from paper_2601_08800_b200 import SwiGLUExperts, _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    n, m = shape
+    T, h, E, I = 96, 256, 16, 256
+    ex = SwiGLUExperts.random(E, h, I, seed=5)
+    w13, w2 = ex.stacked_shards(n, m)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    logits = torch.randn(n * T, E, device="cuda", generator=gen)
+    plan = LayerPlan(n, m, T, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu", inter=I,
+                     wire="token")
+    y = torch.empty(n * T, h, dtype=torch.bfloat16, device="cuda")
+    plan.forward(x, N.ExpertParams(None, None, w13.data_ptr(), w2.data_ptr()), logits=logits,
+                 y_out=y)
+    oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                           ex.w_down.float().cpu().numpy())
+    ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
+    assert orc.verify_metric(y.float().cpu().numpy(), y_o) <= 2e-2
+    plan.close()
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (4, 1)])
+def test_wire_token_f32_affine_emulated(shape):
+    """f32 rows through the bulk-copy pre-reduction (affine experts): within
+    f32 association of the reference layer."""
+    from paper_2601_08800_b200 import RouterSpec, _native as N
+    from paper_2601_08800_b200.plan import LayerPlan
+    n, m = shape
+    T, h, E, k = 48, 64, 16, 4
+    rng = np.random.default_rng(n * 5 + m)
+    x = rng.standard_normal((n * T, h)).astype(np.float32)
+    router = RouterSpec.random(n * T, E, k, seed=n * 3 + m)
+    ids, w = router.arrays()
+    sc = np.linspace(0.5, 1.5, E).astype(np.float32)
+    bi = np.linspace(-0.1, 0.1, E).astype(np.float32)
+    plan = LayerPlan(n, m, T, h, E, k, dtype=torch.float32, wire="token")
+    sct, bit = torch.as_tensor(sc).cuda(), torch.as_tensor(bi).cuda()
+    params = N.ExpertParams(sct.data_ptr(), bit.data_ptr(), None, None)
+    y = torch.empty(n * T, h, dtype=torch.float32, device="cuda")
+    plan.forward(torch.as_tensor(x).cuda(), params, ids=torch.as_tensor(ids).cuda(),
+                 weights=torch.as_tensor(w.astype(np.float32)).cuda(), y_out=y)
+    y_ref, _ = orc.run_fused_affine(n, m, x.astype(np.float64), ids, w, E,
+                                    sc.astype(np.float64), bi.astype(np.float64))
+    assert orc.verify_metric(y.cpu().numpy().astype(np.float64), y_ref) <= 1e-5
+    plan.close()
+
+
 @pytest.mark.parametrize("s_zipf,wire", [(1.2, "token"), (1.2, "slot"), (0.8, "token")])
 def test_zipf_skew_layer_emulated(s_zipf, wire):
     """Config E on the emulated 4x2 cluster: Zipf-skewed gate logits, the
