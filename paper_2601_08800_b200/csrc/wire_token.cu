@@ -192,29 +192,43 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
     skip0 = at<int>(v, v.rank, v.off.poff)[g * v.n + g];
     skip1 = skip0 + at<int>(v, v.rank, v.off.ucnt_all)[g * v.n + g];
   }
-  // warps walk only the pairs left to expand (the own-group block skipped)
+  // warps walk only the pairs left to expand (the own-group block skipped);
+  // lane i holds slot i's row, the next pair's count and rows are loaded
+  // while the current pair is copied, and a lane's whole 4 KB share of the
+  // row (8 x 16 B) is in flight at once
   const long long todo = pairs - (skip1 - skip0);
+  const int KH = v.KH;
+  auto pair_of = [&](long long r) { return r < skip0 ? r : r + (skip1 - skip0); };
+  int cnt = 0, row_l = 0;
+  if (gw < todo) {
+    const long long u = pair_of(gw);
+    cnt = pn[u];
+    if (lane < KH) row_l = pe[u * KH + lane].p;
+  }
   for (long long r = gw; r < todo; r += nwarps) {
-    const long long u = r < skip0 ? r : r + (skip1 - skip0);
-    const int cnt = pn[u];
-    int rows[MX_KMAX];
-    for (int i = 0; i < cnt; ++i) rows[i] = pe[u * v.KH + i].p;
+    const long long u = pair_of(r);
+    int ncnt = 0, nrow_l = 0;
+    if (r + nwarps < todo) {
+      const long long un = pair_of(r + nwarps);
+      ncnt = pn[un];
+      if (lane < KH) nrow_l = pe[un * KH + lane].p;
+    }
     const char* src = xbuf + (size_t)u * row_bytes;
-    size_t o = (size_t)lane * 16;
-    for (; o + 3 * 512 < row_bytes; o += 4 * 512) {  // 4 x 16 B loads in flight per lane
-      uint4 val[4];
+    for (size_t base = 0; base < row_bytes; base += 8 * 512) {  // warp-uniform (shfl below)
+      const size_t o = base + (size_t)lane * 16;
+      uint4 val[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) val[q] = ld_v4(src + o + q * 512);
+      for (int q = 0; q < 8; ++q)
+        if (o + q * 512 < row_bytes) val[q] = ld_v4(src + o + q * 512);
       for (int i = 0; i < cnt; ++i) {
-        char* dst = recv + (size_t)rows[i] * row_bytes + o;
+        char* dst = recv + (size_t)__shfl_sync(0xffffffffu, row_l, i) * row_bytes + o;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) st_v4(dst + q * 512, val[q]);
+        for (int q = 0; q < 8; ++q)
+          if (o + q * 512 < row_bytes) st_v4(dst + q * 512, val[q]);
       }
     }
-    for (; o < row_bytes; o += 512) {
-      const uint4 val = ld_v4(src + o);
-      for (int i = 0; i < cnt; ++i) st_v4(recv + (size_t)rows[i] * row_bytes + o, val);
-    }
+    cnt = ncnt;
+    row_l = nrow_l;
   }
 }
 
