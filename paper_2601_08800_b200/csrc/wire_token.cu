@@ -46,7 +46,7 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 // own group) once per host it hits, then publish per-slot metadata to the TP
 // peer on that host: the pair's packed (slot row, weight) list and its length.
 template <class WT>
-__global__ void __launch_bounds__(256, 3) k_dispatch_token(DevView v, const char* __restrict__ x) {
+__global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char* __restrict__ x) {
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   // DSPLIT warps per token, each moving its slice of the row's 16 B vectors
@@ -74,17 +74,23 @@ __global__ void __launch_bounds__(256, 3) k_dispatch_token(DevView v, const char
   const size_t s_lo = sub * nv_sh / DSPLIT, s_hi = (sub + 1) * nv_sh / DSPLIT;
   for (long long t = gw / DSPLIT; t < v.T; t += nwarps / DSPLIT) {
     const char* row = x + (size_t)t * row_bytes;
+    // the token's routing, one load round: lane d holds its pair row on host
+    // d, lane i (< k) slot i's expert, host, RECV row and weight
+    const int u_l = lane < n ? upos[t * n + lane] : -1;
+    int e_l = 0, d_l = -1, p_l = 0;
+    WT w_l = 0;
+    if (lane < k) {
+      e_l = ids[t * k + lane];
+      d_l = home_of(e_l, n, E);
+      p_l = slot_pos[t * k + lane];
+      if (sub == 0) w_l = wts[t * k + lane];
+    }
     for (int d = 0; d < n; ++d) {
-      const int u = upos[t * n + d];
+      const int u = __shfl_sync(0xffffffffu, u_l, d);
       if (u < 0) continue;
       if (d == v.group && direct_local) {
         // rows of this token's slots on the own host (pos < cap: layout-checked)
-        int pos = -1;
-        if (lane < k) {
-          const int e = ids[t * k + lane];
-          const int p = slot_pos[t * k + lane];
-          if (home_of(e, n, E) == d && p < v.cap) pos = p;
-        }
+        const int pos = (d_l == d && p_l < v.cap) ? p_l : -1;
         const unsigned mine = __ballot_sync(0xffffffffu, pos >= 0);
         char* recv = at<char>(v, v.rank, v.off.recv);
         // warp-uniform passes (the slot broadcast below is a full-warp
@@ -138,11 +144,8 @@ __global__ void __launch_bounds__(256, 3) k_dispatch_token(DevView v, const char
     }
     if (sub != 0) continue;
     // metadata: lane i carries slot i
-    int e = 0, d = -1;
-    if (lane < k) {
-      e = ids[t * k + lane];
-      d = home_of(e, n, E);
-    }
+    const int e = e_l, d = d_l;
+    const int ud = __shfl_sync(0xffffffffu, u_l, d < 0 ? 0 : d);
     int idx = 0, cnt = 0;
     for (int o = 0; o < k; ++o) {
       const int oe = __shfl_sync(0xffffffffu, e, o);
@@ -153,12 +156,11 @@ __global__ void __launch_bounds__(256, 3) k_dispatch_token(DevView v, const char
       }
     }
     if (lane < k) {
-      const int u = upos[t * n + d];
-      const int p = slot_pos[t * k + lane];
+      const int u = ud;
       const int dst = d * m + v.tp_rank;  // the TP peer that reads this metadata
       PairEnt<WT> ent;
-      ent.p = p;
-      ent.w = wts[t * k + lane];
+      ent.p = p_l;
+      ent.w = w_l;
       reinterpret_cast<PairEnt<WT>*>(at<char>(v, dst, v.off.pair_p))[(size_t)u * v.KH + idx] = ent;
       if (idx == 0) {
         at<int>(v, dst, v.off.pair_n)[u] = cnt;
