@@ -596,67 +596,70 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
   const int sw = (h + m - 1) / m;
   const T* zin = at<T>(v, v.rank, v.off.zin) - c0;
   for (long long t = gw; t < v.T; t += nwarps) {
-    int hs[HMAX], nh = 0;
-    for (int i = 1; i <= n; ++i) {
-      const int d = (j - i + n) % n;  // arrival order j-1, ..., j
-      const int u = upos[t * n + d];
-      if (u >= 0 && nh < HMAX) hs[nh++] = d;
+    // lane l: the token's pair on host j-1-l (arrival order j-1, ..., j),
+    // all n loaded in one round
+    int u_l = -1;
+    if (lane < n) u_l = upos[t * n + (j - (lane + 1) + n) % n];
+    const unsigned hm = __ballot_sync(0xffffffffu, u_l >= 0);
+    const int nh = __popc(hm);
+    int hs[HMAX];
+    {
+      unsigned bits = hm;
+#pragma unroll
+      for (int a = 0; a < HMAX; ++a) {
+        hs[a] = bits ? (j - __ffs(bits) + n) % n : 0;
+        bits &= bits - 1;
+      }
     }
     int c = c0 + lane * V;
     if (m * nh <= 4) {
-      // fast path: every (host TP rank, host) ZIN load of two column vectors
-      // is issued before any is consumed; the sum keeps the TP-rank-major,
-      // arrival-order association
+      // fast path: every (host TP rank, host) ZIN load of CG column
+      // vectors is issued before any is consumed; the sum keeps the
+      // TP-rank-major, arrival-order association
       const T* src[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int tt = i / (nh > 0 ? nh : 1), a = i % (nh > 0 ? nh : 1);
-        src[i] = i < m * nh ? zin + (((size_t)hs[a] * m + tt) * v.T + t) * sw : nullptr;
+        int ha = hs[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q)
+          if (q == a) ha = hs[q];
+        src[i] = i < m * nh ? zin + (((size_t)ha * m + tt) * v.T + t) * sw : nullptr;
       }
-      for (; c + 32 * V < c1; c += 64 * V) {
-        uint4 r0[4], r1[4];
+      constexpr int CG = 2;
+      for (; c + (CG - 1) * 32 * V < c1; c += CG * 32 * V) {
+        uint4 r[4][CG];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (i < m * nh) {
-            r0[i] = ld_v4(src[i] + c);
-            r1[i] = ld_v4(src[i] + c + 32 * V);
-          }
-        A a0[V], a1[V];
+          if (i < m * nh)
 #pragma unroll
-        for (int q = 0; q < V; ++q) a0[q] = a1[q] = (A)0;
+            for (int g = 0; g < CG; ++g) r[i][g] = ld_v4(src[i] + c + g * 32 * V);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i < m * nh) {
-            const T* p0 = reinterpret_cast<const T*>(&r0[i]);
-            const T* p1 = reinterpret_cast<const T*>(&r1[i]);
+        for (int g = 0; g < CG; ++g) {
+          A acc[V];
 #pragma unroll
-            for (int q = 0; q < V; ++q) {
-              a0[q] = add_rn(a0[q], to_acc(p0[q]));
-              a1[q] = add_rn(a1[q], to_acc(p1[q]));
+          for (int q = 0; q < V; ++q) acc[q] = (A)0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i < m * nh) {
+              const T* pv = reinterpret_cast<const T*>(&r[i][g]);
+#pragma unroll
+              for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
             }
-          }
-        if (v.Is_t)
-          for (int tt = 0; tt < m; ++tt) {
-            const T* ps = at<T>(v, j * m + tt, v.off.part_s) + (size_t)t * h + c;
-            const uint4 s0 = ld_v4(ps), s1 = ld_v4(ps + 32 * V);
-            const T* q0 = reinterpret_cast<const T*>(&s0);
-            const T* q1 = reinterpret_cast<const T*>(&s1);
+          const int cg = c + g * 32 * V;
+          if (v.Is_t)
+            for (int tt = 0; tt < m; ++tt) {
+              const uint4 sraw = ld_v4(at<T>(v, j * m + tt, v.off.part_s) + (size_t)t * h + cg);
+              const T* pv = reinterpret_cast<const T*>(&sraw);
 #pragma unroll
-            for (int q = 0; q < V; ++q) {
-              a0[q] = add_rn(a0[q], to_acc(q0[q]));
-              a1[q] = add_rn(a1[q], to_acc(q1[q]));
+              for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
             }
-          }
-        T o0[V], o1[V];
+          T out[V];
 #pragma unroll
-        for (int q = 0; q < V; ++q) {
-          o0[q] = from_acc<T>(a0[q]);
-          o1[q] = from_acc<T>(a1[q]);
-        }
-        for (int tt = 0; tt < m; ++tt) {
-          T* y = at<T>(v, j * m + tt, v.off.y) + (size_t)t * h + c;
-          st_v4(y, *reinterpret_cast<uint4*>(o0));
-          st_v4(y + 32 * V, *reinterpret_cast<uint4*>(o1));
+          for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+          for (int tt = 0; tt < m; ++tt)
+            st_v4(at<T>(v, j * m + tt, v.off.y) + (size_t)t * h + cg,
+                  *reinterpret_cast<uint4*>(out));
         }
       }
     }
