@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(256, 1) k_pair_reduce(DevView v) {
 // CTA per SM, 12% warps active, 51 us for one config-B rank's 134 MB on the
 // emulated cluster (tools/emu_layer.py under ncu).  Here the TMA engine
 // streams the rows into a ring of row slots in shared memory and registers
-// only hold the sums (43-45 us emulated; 59.8 vs 62.6-66 us inside the 4-GPU
+// only hold the sums (43-46 us emulated; 59.8 vs 62.6-66 us inside the 4-GPU
 // layer, where the NVLink pushes bound it):
 //   warp 0      producer: walks the CTA's contiguous range of pairs, four at
 //               a time (lane l: entry l&7 of pair l>>3, two batches ahead),
