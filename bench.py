@@ -36,6 +36,9 @@ sys.path.insert(0, str(ROOT))
 
 H, INTER, E, K_TOP, T_GLOBAL = 2048, 768, 128, 8, 8192
 NVLINK_PEER_GBS = 770.0      # measured peer copy, B200_PROFILING.md
+# what SM-issued 16 B peer stores of 4 KB rows reach on 4 B200s (every GPU
+# pushing at once; tools/nvlink_bench.py -> profiles/r01_nvlink_ceiling_n4.jsonl)
+NVLINK_SM_STORE_GBS = 680.0
 HBM_REF_GBS = 6539.5         # MEASURED_PEAKS.json copy bandwidth (bound selection only)
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -544,6 +547,10 @@ def run_ours(args):
             peak_src = "NVLink peer copy 770 GB/s/direction (B200_PROFILING.md)"
         rooflines[ph] = {"bound": spec["bound"], "achieved": ach, "peak": peak, "unit": unit,
                          "frac": ach / peak, "us": avg[ph] * 1e3, "peak_source": peak_src}
+        if spec["bound"] == "nvlink":
+            rooflines[ph]["frac_sm_store_ceiling"] = ach / NVLINK_SM_STORE_GBS
+            rooflines[ph]["sm_store_ceiling_source"] = (
+                f"{NVLINK_SM_STORE_GBS:.0f} GB/s, profiles/r01_nvlink_ceiling_n4.jsonl")
     kernels = {k: v for k, v in rooflines.items()}
     dom = max(kernels, key=lambda k: kernels[k]["us"]) if kernels else None
     traffic = None

@@ -236,9 +236,22 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
 
 // Destination of column c of pair-reduced row z (owner token tok = j*T + t)
 // in the owner's shard: TP rank tt of group j owns columns [c0, c1) and keeps
-// one [T][sw] plane per (host, host TP rank) in its ZIN.  A lane's columns
-// only grow along a row, so the cursor advances the shard incrementally
-// (no division or shard search per store).
+// one [T][sw] plane per (host, host TP rank) in its ZIN.
+template <class T>
+__device__ __forceinline__ T* zin_dst(const DevView& v, int tok, int c, int sw) {
+  const int j = tok / v.T, t = tok - j * v.T;
+  int tt = 0, c0 = 0, c1 = 0;
+  for (; tt < v.m; ++tt) {
+    col_shard(v.h, v.m, tt, &c0, &c1);
+    if (c < c1) break;
+  }
+  return at<T>(v, j * v.m + tt, v.off.zin) +
+         (((size_t)v.group * v.m + v.tp_rank) * v.T + t) * sw + (c - c0);
+}
+
+// The bulk-copy kernel's form: a lane's columns only grow along a row, so
+// the cursor advances the shard incrementally (no division or shard search
+// per store).
 template <class T>
 struct ZinCursor {
   int j, tt, c0, c1;
@@ -267,61 +280,13 @@ struct ZinCursor {
 // combine fused into the pre-reduction: the owner then only reads local
 // memory); all slot loads of a column vector are issued before use.
 
-template <int DT, class WT, int CV, int KR>
-__device__ __forceinline__ void pair_rows(const DevView& v, const typename Elt<DT>::T* part,
-                                          const int* prow, const typename Elt<DT>::Acc* w,
-                                          int cnt, int tok, int lane) {
-  // CV column vectors per lane per round, all cnt (<= KR) slot loads of a
-  // round issued before use
-  using T = typename Elt<DT>::T;
-  using A = typename Elt<DT>::Acc;
-  constexpr int V = Elt<DT>::V;
-  const int h = v.h, sw = (h + v.m - 1) / v.m;
-  ZinCursor<T> zc(v, tok, sw);
-  for (int c = lane * V; c < h; c += CV * 32 * V) {
-    uint4 raw[CV][KR];
-#pragma unroll
-    for (int i = 0; i < KR; ++i)
-      if (i < cnt)
-#pragma unroll
-        for (int cv = 0; cv < CV; ++cv)
-          if (c + cv * 32 * V < h)
-            raw[cv][i] = ld_v4(part + (size_t)prow[i] * h + c + cv * 32 * V);
-#pragma unroll
-    for (int cv = 0; cv < CV; ++cv) {
-      if (c + cv * 32 * V >= h) break;
-      A acc[V];
-#pragma unroll
-      for (int q = 0; q < V; ++q) acc[q] = (A)0;
-#pragma unroll
-      for (int i = 0; i < KR; ++i)
-        if (i < cnt) {
-          const T* pv = reinterpret_cast<const T*>(&raw[cv][i]);
-#pragma unroll
-          for (int q = 0; q < V; ++q) {
-            if constexpr (DT == MX_F64)  // reference association, uncontracted
-              acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
-            else
-              acc[q] = fmaf(w[i], to_acc(pv[q]), acc[q]);
-          }
-        }
-      T out[V];
-#pragma unroll
-      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-      st_v4(zc(v, c + cv * 32 * V), *reinterpret_cast<uint4*>(out));
-    }
-  }
-}
-
-// Persistent warps walk the host's pairs; the next pair's count, owner and
-// slot entries (lane i holds entry i) are loaded while the current pair's
-// rows are reduced, so only the row loads sit on each pair's critical path.
 template <int DT, class WT>
-__global__ void __launch_bounds__(256, 1) k_pair_reduce(DevView v) {
+__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
+  constexpr int KU = 8;
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -331,55 +296,67 @@ __global__ void __launch_bounds__(256, 1) k_pair_reduce(DevView v) {
   const T* part = at<T>(v, v.rank, v.off.partial);
   const int* ptok = at<int>(v, v.rank, v.off.pair_tok);
   const int h = v.h, sw = (h + v.m - 1) / v.m;
-  int cnt = 0, tok = 0;
-  PairEnt<WT> ent{};
-  if (gw < pairs) {
-    cnt = pn[gw];
-    tok = ptok[gw];
-    if (lane < v.KH) ent = pe[gw * v.KH + lane];
-  }
   for (long long u = gw; u < pairs; u += nwarps) {
-    const long long un = u + nwarps;
-    int ncnt = 0, ntok = 0;
-    PairEnt<WT> nent{};
-    if (un < pairs) {
-      ncnt = pn[un];
-      ntok = ptok[un];
-      if (lane < v.KH) nent = pe[un * v.KH + lane];
+    const int cnt = pn[u];
+    const int tok = ptok[u];
+    const T* rp[KU];
+    A w[KU];
+#pragma unroll
+    for (int i = 0; i < KU; ++i) {
+      const PairEnt<WT> e = pe[u * v.KH + (i < cnt ? i : 0)];
+      rp[i] = part + (size_t)e.p * h;
+      w[i] = (A)e.w;
     }
-    if (cnt <= 8) {
-      int prow[8];
-      A w[8];
+    int c = lane * V;
+    if (cnt <= KU) {
+      for (; c + 32 * V < h; c += 64 * V) {  // two column vectors per lane: 2 x cnt loads in flight
+        uint4 raw[2][KU];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int src = i < cnt ? i : 0;
-        prow[i] = __shfl_sync(0xffffffffu, ent.p, src);
-        w[i] = (A)__shfl_sync(0xffffffffu, ent.w, src);
-      }
-      if (cnt <= 4) pair_rows<DT, WT, 4, 4>(v, part, prow, w, cnt, tok, lane);
-      else pair_rows<DT, WT, 2, 8>(v, part, prow, w, cnt, tok, lane);
-    } else {
-      ZinCursor<T> zc(v, tok, sw);
-      for (int c = lane * V; c < h; c += 32 * V) {
-        A acc[V];
+        for (int i = 0; i < KU; ++i)
+          if (i < cnt) {
+            raw[0][i] = ld_v4(rp[i] + c);
+            raw[1][i] = ld_v4(rp[i] + c + 32 * V);
+          }
 #pragma unroll
-        for (int q = 0; q < V; ++q) acc[q] = (A)0;
-        for (int i = 0; i < cnt; ++i) {
-          const PairEnt<WT> e = pe[u * v.KH + i];
-          const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
-          const T* pv = reinterpret_cast<const T*>(&raw);
+        for (int hh = 0; hh < 2; ++hh) {
+          A acc[V];
 #pragma unroll
-          for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
+          for (int q = 0; q < V; ++q) acc[q] = (A)0;
+#pragma unroll
+          for (int i = 0; i < KU; ++i)
+            if (i < cnt) {
+              const T* pv = reinterpret_cast<const T*>(&raw[hh][i]);
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                if constexpr (DT == MX_F64)  // reference association, uncontracted
+                  acc[q] = add_rn(acc[q], mul_rn(w[i], to_acc(pv[q])));
+                else
+                  acc[q] = fmaf(w[i], to_acc(pv[q]), acc[q]);
+              }
+            }
+          T out[V];
+#pragma unroll
+          for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+          st_v4(zin_dst<T>(v, tok, c + hh * 32 * V, sw), *reinterpret_cast<uint4*>(out));
         }
-        T out[V];
-#pragma unroll
-        for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-        st_v4(zc(v, c), *reinterpret_cast<uint4*>(out));
       }
     }
-    cnt = ncnt;
-    tok = ntok;
-    ent = nent;
+    for (; c < h; c += 32 * V) {
+      A acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = (A)0;
+      for (int i = 0; i < cnt; ++i) {
+        const PairEnt<WT> e = pe[u * v.KH + i];
+        const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+        const T* pv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
+      }
+      T out[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+      st_v4(zin_dst<T>(v, tok, c, sw), *reinterpret_cast<uint4*>(out));
+    }
   }
   if (v.sync_signal) grid_signal(v);  // every owner's ZIN written: barrier #3
 }
@@ -764,7 +741,11 @@ int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
 
 int launch_pair_reduce(const DevView& v, cudaStream_t s) {
   const size_t row_bytes = (size_t)v.h * v.elt;
-  if (v.elt != 8 && v.T > 0 && prb_slots(row_bytes) >= PRB_KU) {
+  // The ring pays off for short pairs (k/n slots per pair on average):
+  // config B, 4 GPUs (k/n = 4) 60.1 vs 62.6-66 us in the layer.  With one
+  // host (n = 1: every pair holds all k slots) the register kernel is
+  // faster: 67.6 vs 90.3 us at 2 GPUs, k = 8.
+  if (v.elt != 8 && v.T > 0 && v.k <= 4 * v.n && prb_slots(row_bytes) >= PRB_KU) {
     auto kern = v.elt == 4 ? k_pair_reduce_bulk<MX_F32> : k_pair_reduce_bulk<MX_BF16>;
     static bool attr[2] = {false, false};
     if (!attr[v.elt == 4]) {
@@ -778,9 +759,8 @@ int launch_pair_reduce(const DevView& v, cudaStream_t s) {
     MX_LAUNCH_CHECK();
     return MX_OK;
   }
-  // f64 (reference association) and rows too wide to stage: register kernel
-  int g = blocks_for((long long)v.T * v.n);
-  if (g > 148) g = 148;  // persistent, one CTA per SM
+  // f64 (reference association), long pairs, rows too wide to stage
+  const int g = blocks_for((long long)v.T * v.n);
   switch (v.elt) {
     case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, 256, 0, s, v); break;
     case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, 256, 0, s, v); break;

@@ -565,20 +565,24 @@ def test_wire_token_swiglu_emulated(shape):
     plan.close()
 
 
-@pytest.mark.parametrize("shape,k", [((2, 2), 12), ((1, 2), 12), ((4, 1), 6)])
-def test_wire_token_pair_reduce_slot_counts(shape, k):
-    """The bulk-copy pre-reduction stages pairs of at most 8 slots in shared
-    memory and reads larger pairs straight from HBM: top-k 12 mixes both
-    (all pairs exceed 8 slots on one host)."""
+@pytest.mark.parametrize("shape,k,E,hot", [((2, 2), 4, 16, False), ((4, 1), 12, 48, True),
+                                           ((2, 2), 12, 16, False), ((1, 2), 12, 16, False)])
+def test_wire_token_pair_reduce_slot_counts(shape, k, E, hot):
+    """Both pre-reductions: the bulk-copy ring for short pairs (k <= 4n; it
+    stages pairs of at most 8 slots and reads longer ones straight from HBM
+    -- ``hot`` routes half the tokens to all 12 experts of host 0) and the
+    register kernel for long pairs (k > 4n)."""
     from paper_2601_08800_b200 import SwiGLUExperts, _native as N
     from paper_2601_08800_b200.plan import LayerPlan
     n, m = shape
-    T, h, E, I = 96, 256, 16, 256
+    T, h, I = 96, 256, 256
     ex = SwiGLUExperts.random(E, h, I, seed=5)
     w13, w2 = ex.stacked_shards(n, m)
     gen = torch.Generator(device="cuda").manual_seed(9)
     x = torch.randn(n * T, h, device="cuda", generator=gen).to(torch.bfloat16)
     logits = torch.randn(n * T, E, device="cuda", generator=gen)
+    if hot:
+        logits[: n * T // 2, : E // n] += 8.0
     plan = LayerPlan(n, m, T, h, E, k, dtype=torch.bfloat16, expert_kind="swiglu", inter=I,
                      wire="token")
     y = torch.empty(n * T, h, dtype=torch.bfloat16, device="cuda")
@@ -587,6 +591,9 @@ def test_wire_token_pair_reduce_slot_counts(shape, k):
     oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
                            ex.w_down.float().cpu().numpy())
     ids, w = orc.router_topk(logits.cpu().numpy(), k)
+    if hot:
+        on0 = ((ids * n) // E == 0).sum(axis=1)
+        assert on0.max() > 8  # some pairs exceed the staged 8 slots
     y_o = orc.moe_layer_swiglu(x.float().cpu().numpy(), ids, w, oex)
     assert orc.verify_metric(y.float().cpu().numpy(), y_o) <= 2e-2
     plan.close()
