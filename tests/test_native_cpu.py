@@ -99,3 +99,20 @@ def test_malformed_trace_row_names_its_line():
             "0,0,route,local,oops,0,,compute,1,0.0\n")
     with pytest.raises(ValueError, match="line 2"):
         trace_from_csv(text)
+
+
+def test_nvlink_diagnostic_kernels_build_for_sm100a():
+    """tools/nvlink_push.cu (the NVLink ceiling bench's kernels) stays
+    buildable for sm_100a; nvcc cross-compiles without a GPU."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(nvcc).exists():
+        pytest.skip("nvcc not available")
+    out = ROOT / "paper_2601_08800_b200" / "csrc" / "build" / "nvlink_push_check.so"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    subprocess.run([nvcc, "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                    "-Xcompiler", "-fPIC", str(ROOT / "tools" / "nvlink_push.cu"), "-o", str(out)],
+                   check=True, capture_output=True)
+    lib = C.CDLL(str(out))
+    assert hasattr(lib, "nb_launch") and hasattr(lib, "nb_enable_peers")
