@@ -741,21 +741,21 @@ int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
 
 int launch_pair_reduce(const DevView& v, cudaStream_t s) {
   const size_t row_bytes = (size_t)v.h * v.elt;
-  // The ring pays off for short pairs (k/n slots per pair on average):
-  // config B, 4 GPUs (k/n = 4) 60.1 vs 62.6-66 us in the layer.  With one
-  // host (n = 1: every pair holds all k slots) the register kernel is
-  // faster: 67.6 vs 90.3 us at 2 GPUs, k = 8.
-  if (v.elt != 8 && v.T > 0 && v.k <= 4 * v.n && prb_slots(row_bytes) >= PRB_KU) {
+  // The ring pays off for many short pairs (k/n slots per pair on
+  // average): config B, 4 GPUs (k/n = 4) 60.1 vs 62.6-66 us in the layer.
+  // With one host (n = 1: every pair holds all k slots) the register kernel
+  // is faster: 67.6 vs 90.3 us at 2 GPUs, k = 8.  Batches too small to give
+  // every SM 32 pairs (decode) keep the register kernel's single latency
+  // chain per pair.
+  if (v.elt != 8 && v.k <= 4 * v.n && (long long)v.T * v.n >= 148LL * 32 &&
+      prb_slots(row_bytes) >= PRB_KU) {
     auto kern = v.elt == 4 ? k_pair_reduce_bulk<MX_F32> : k_pair_reduce_bulk<MX_BF16>;
     static bool attr[2] = {false, false};
     if (!attr[v.elt == 4]) {
       MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr[v.elt == 4] = true;
     }
-    long long g = ((long long)v.T * v.n + 31) / 32;  // >= 32 pairs per CTA
-    if (g > 148) g = 148;
-    if (g < 1) g = 1;
-    pdl_launch(kern, (int)g, PRB_WARPS * 32, prb_smem(row_bytes), s, v);
+    pdl_launch(kern, 148, PRB_WARPS * 32, prb_smem(row_bytes), s, v);  // one CTA per SM
     MX_LAUNCH_CHECK();
     return MX_OK;
   }

@@ -565,17 +565,20 @@ def test_wire_token_swiglu_emulated(shape):
     plan.close()
 
 
-@pytest.mark.parametrize("shape,k,E,hot", [((2, 2), 4, 16, False), ((4, 1), 12, 48, True),
-                                           ((2, 2), 12, 16, False), ((1, 2), 12, 16, False)])
-def test_wire_token_pair_reduce_slot_counts(shape, k, E, hot):
-    """Both pre-reductions: the bulk-copy ring for short pairs (k <= 4n; it
-    stages pairs of at most 8 slots and reads longer ones straight from HBM
-    -- ``hot`` routes half the tokens to all 12 experts of host 0) and the
-    register kernel for long pairs (k > 4n)."""
+@pytest.mark.parametrize("shape,k,E,hot,T", [((2, 2), 4, 16, False, 2560),
+                                             ((4, 1), 12, 48, True, 1280),
+                                             ((2, 2), 12, 16, False, 2560),
+                                             ((1, 2), 12, 16, False, 96)])
+def test_wire_token_pair_reduce_slot_counts(shape, k, E, hot, T):
+    """Both pre-reductions: the bulk-copy ring for many short pairs (k <= 4n
+    and T*n >= 148*32; it stages pairs of at most 8 slots and reads longer
+    ones straight from HBM -- ``hot`` routes half the tokens to all 12
+    experts of host 0) and the register kernel for long pairs (k > 4n) or
+    small batches."""
     from paper_2601_08800_b200 import SwiGLUExperts, _native as N
     from paper_2601_08800_b200.plan import LayerPlan
     n, m = shape
-    T, h, I = 96, 256, 256
+    h, I = 256, 256
     ex = SwiGLUExperts.random(E, h, I, seed=5)
     w13, w2 = ex.stacked_shards(n, m)
     gen = torch.Generator(device="cuda").manual_seed(9)
@@ -599,14 +602,14 @@ def test_wire_token_pair_reduce_slot_counts(shape, k, E, hot):
     plan.close()
 
 
-@pytest.mark.parametrize("shape", [(2, 2), (4, 1)])
-def test_wire_token_f32_affine_emulated(shape):
-    """f32 rows through the bulk-copy pre-reduction (affine experts): within
-    f32 association of the reference layer."""
+@pytest.mark.parametrize("shape,T", [((2, 2), 48), ((4, 1), 1280)])
+def test_wire_token_f32_affine_emulated(shape, T):
+    """f32 rows through both pre-reductions (affine experts; the bulk-copy
+    ring at 4 x 1280 tokens): within f32 association of the reference."""
     from paper_2601_08800_b200 import RouterSpec, _native as N
     from paper_2601_08800_b200.plan import LayerPlan
     n, m = shape
-    T, h, E, k = 48, 64, 16, 4
+    h, E, k = 64, 16, 4
     rng = np.random.default_rng(n * 5 + m)
     x = rng.standard_normal((n * T, h)).astype(np.float32)
     router = RouterSpec.random(n * T, E, k, seed=n * 3 + m)
