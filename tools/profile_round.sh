@@ -4,8 +4,9 @@
 # Writes everything under gpurun_out/<tag>_*: bench lines at 1/2/4 GPUs, the
 # reference arm, the N=1 ncu launch list, ncu --set full captures of the
 # grouped GEMMs and the N=1 memory kernels, the N=4/N=2 GEMM shapes under
-# ncu (DRAM traffic per launch), config C/E sweeps, decode sweeps and the
-# measured trace.  Every ncu command runs only after the same command has
+# ncu (DRAM traffic per launch), the token-wire memory kernels of one rank on
+# the emulated cluster under ncu, the SM-issued NVLink ceiling, config C/E
+# sweeps, decode sweeps and the measured trace.  Every ncu command runs only after the same command has
 # exited 0 without ncu; multi-rank commands are never run under ncu.
 set -u
 TAG=${1:-r01}
@@ -48,6 +49,17 @@ for shape in "n4 64 768 2048 --swiglu" "n4 64 2048 384" "n2 128 768 2048 --swigl
     echo "ncu gemm $key N=$NN K=$KK rc=$?"
   fi
 done
+
+# token-wire memory kernels of one config-B rank (emulated cluster, one GPU)
+if CUDA_VISIBLE_DEVICES=0 timeout 120 python tools/emu_layer.py > /dev/null 2>&1; then
+  CUDA_VISIBLE_DEVICES=0 timeout 300 ncu --set full --clock-control none --import-source on \
+    -k "regex:k_pair_reduce|k_expand|k_dispatch_token|k_combine_token" -s 16 -c 8 \
+    -o $OUT/${TAG}_emu_token python tools/emu_layer.py > /dev/null 2>&1
+  echo "ncu emu token rc=$?"
+fi
+# what SM-issued peer stores / loads reach (all GPUs of the box at once)
+timeout 200 python tools/nvlink_bench.py --out $OUT/${TAG}_nvlink_ceiling.jsonl > /dev/null 2>&1
+echo "nvlink ceiling rc=$?"
 
 timeout 600 $TR --nproc-per-node 4 --master-port 29681 tools/config_sweep.py --config C \
   --out $OUT/${TAG}_configC_n4.jsonl > $OUT/${TAG}_configC.log 2>&1
