@@ -362,13 +362,14 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
 }
 
 // Bulk-copy pre-reduction (bf16 / f32 rows, at most 8 slots per pair read
-// from shared memory; larger pairs straight from HBM).  The register kernel
-// above keeps only as many slot rows in flight as its registers hold -- one
-// CTA per SM, 12% warps active, 51 us for one config-B rank's 134 MB on the
-// emulated cluster (tools/emu_layer.py under ncu).  Here the TMA engine
-// streams the rows into a ring of row slots in shared memory and registers
-// only hold the sums (43-46 us emulated; 59.8 vs 62.6-66 us inside the 4-GPU
-// layer, where the NVLink pushes bound it):
+// from shared memory; larger pairs straight from HBM).  A register-only
+// kernel keeps only as many slot rows in flight as its registers hold (a
+// persistent variant at one CTA per SM: 12% warps active, 51 us for one
+// config-B rank's 134 MB on the emulated cluster, tools/emu_layer.py under
+// ncu).  Here the TMA engine streams the rows into a ring of row slots in
+// shared memory and registers only hold the sums (43-46 us emulated; 60.1
+// vs 66-67 us for the register kernel above inside the 4-GPU layer, where
+// the NVLink pushes bound it):
 //   warp 0      producer: walks the CTA's contiguous range of pairs, four at
 //               a time (lane l: entry l&7 of pair l>>3, two batches ahead),
 //               writes each pair's header (count, owner token, first slot,
