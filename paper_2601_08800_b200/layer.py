@@ -25,9 +25,24 @@ from .plan import LayerPlan, stream_ptr
 from .simcluster import FP8SwiGLUExperts, SwiGLUExperts
 
 
-def layout_for(world: int, tp: int | None = None):
+def layout_for(world: int, tp: int | str | None = None, *, routing=None, num_experts=None,
+               hidden=None, inter=None, calib=None):
     """(n_group, tp) for a world size; default keeps TP=2 (config B,
-    TP2 x EP4 at 8 GPUs) and falls back to pure TP/EP for 1 GPU."""
+    TP2 x EP4 at 8 GPUs) and falls back to pure TP/EP for 1 GPU.
+
+    ``tp="auto"``: the layout :func:`.layer_model.select_layout` ranks first
+    for a routing sample -- ``routing`` the [T_global, k] expert ids of a
+    representative batch, identical on every rank (e.g. all-gathered), and
+    the expert shapes.  On one NVSwitch box that is EP-only for a uniform
+    router and TP2 x EP for a skewed one (config E)."""
+    if tp == "auto":
+        if routing is None or None in (num_experts, hidden, inter):
+            raise ValueError("tp='auto' needs routing, num_experts, hidden and inter")
+        from .layer_model import select_layout
+        ranked = select_layout(routing, world, num_experts, hidden, inter, calib)
+        if not ranked:
+            raise ValueError(f"no layout of {world} GPUs fits these expert shapes")
+        return ranked[0]["n"], ranked[0]["m"]
     if tp is None:
         tp = 1 if world == 1 else 2
     if world % tp:

@@ -136,7 +136,7 @@ def predict_layer(ids, n: int, m: int, num_experts: int, hidden: int, inter: int
         seg["combine"] = max(seg["combine"], comb)
     fixed = c.route_layout_us * 1e-6 + (4 * c.barrier_us * 1e-6 if W > 1 else 0.0)
     total = fixed + seg["pre"] + seg["expert"] + seg["combine"]
-    return {"layout": f"TP{m}xEP{n}", "seconds": total, "fixed_s": fixed,
+    return {"layout": f"TP{m}xEP{n}", "n": n, "m": m, "seconds": total, "fixed_s": fixed,
             "segments_s": seg, "host_slots_max": int(S.sum(axis=0).max())}
 
 

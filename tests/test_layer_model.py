@@ -69,3 +69,14 @@ def test_calibration_interpolates_gemm_efficiency():
     g1, g2 = c.gemm(576)
     assert 0.67 < g1 < 0.83 and 0.60 < g2 < 0.73
     assert c.gemm(192) == c.gemm(384) and c.gemm(2048) == c.gemm(768)
+
+
+@pytest.mark.parametrize("s,layout", [(0.0, (4, 1)), (1.2, (2, 2))])
+def test_layout_for_auto_follows_the_model(s, layout):
+    from paper_2601_08800_b200.layer import layout_for
+    assert layout_for(4, "auto", routing=_ids(s), num_experts=E, hidden=H, inter=I) == layout
+    assert layout_for(4) == (2, 2)                       # default: config B's TP2
+    with pytest.raises(ValueError):
+        layout_for(4, "auto")
+    with pytest.raises(ValueError):                      # no TP shard of I=200 is 128-aligned
+        layout_for(4, "auto", routing=_ids(s), num_experts=E, hidden=H, inter=200)
