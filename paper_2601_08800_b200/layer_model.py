@@ -52,6 +52,47 @@ class LayerCalibration:
     route_layout_us: float = 32.0
     barrier_us: float = 6.0   # graph replay: ~5 us intrinsic (barrier_bench) + skew
 
+    # bench.py phase (and the bound it was judged against) -> efficiency key
+    _PHASE_EFF = {("dispatch", "nvlink"): "dispatch_nvlink", ("dispatch", "hbm"): "dispatch_hbm",
+                  ("expand", "hbm"): "expand", ("pair_reduce", "hbm"): "pair_reduce",
+                  ("pair_reduce", "nvlink"): "pair_push_nvlink",
+                  ("combine", "nvlink"): "combine_nvlink", ("combine", "hbm"): "combine_hbm"}
+
+    @classmethod
+    def from_bench(cls, lines, base: "LayerCalibration | None" = None) -> "LayerCalibration":
+        """Recalibrate from measured ``bench.py`` JSON lines (a dict or a
+        list; later lines win): every phase's achieved / peak becomes its
+        efficiency, the GEMM fractions are filed under the line's TP shard
+        ``I/m``, route + layout is the measured latency, and the peaks are
+        the ones the line was judged against.  The device barriers keep
+        ``base``'s figure (phase-mode barriers carry event-node overhead)."""
+        c = base or cls()
+        if isinstance(lines, dict):
+            lines = [lines]
+        eff, gemm_eff = dict(c.eff), dict(c.gemm_eff)
+        hbm, nvl, tf, rl = c.hbm_gbs, c.nvlink_gbs, c.bf16_tflops, c.route_layout_us
+        for line in lines:
+            roof = line.get("rooflines", {})
+            cfg = line.get("config", {})
+            for ph, r in roof.items():
+                key = cls._PHASE_EFF.get((ph, r["bound"]))
+                if key:
+                    eff[key] = float(r["frac"])
+                if r["bound"] == "hbm":
+                    hbm = float(r["peak"])
+                elif r["bound"] == "nvlink":
+                    nvl = float(r["peak"])
+                elif r["bound"] == "tensor":
+                    tf = float(r["peak"])
+            if "gemm1_swiglu" in roof and "gemm2" in roof and cfg.get("moe_intermediate"):
+                shard = int(cfg["moe_intermediate"]) // int(cfg.get("tp_m", 1))
+                gemm_eff[shard] = (float(roof["gemm1_swiglu"]["frac"]), float(roof["gemm2"]["frac"]))
+            ph_us = line.get("phases_us", {})
+            if "route" in ph_us and "layout" in ph_us:
+                rl = float(ph_us["route"]) + float(ph_us["layout"])
+        return cls(hbm_gbs=hbm, nvlink_gbs=nvl, bf16_tflops=tf, gemm_eff=gemm_eff, eff=eff,
+                   route_layout_us=rl, barrier_us=c.barrier_us)
+
     def gemm(self, shard: int):
         ks = sorted(self.gemm_eff)
         if shard <= ks[0]:

@@ -80,3 +80,29 @@ def test_layout_for_auto_follows_the_model(s, layout):
         layout_for(4, "auto")
     with pytest.raises(ValueError):                      # no TP shard of I=200 is 128-aligned
         layout_for(4, "auto", routing=_ids(s), num_experts=E, hidden=H, inter=200)
+
+
+def test_calibration_from_measured_bench_lines():
+    """Recalibrating from the round's bench lines reproduces the defaults
+    (which were read off them) and tracks the newer 4-GPU kernels."""
+    import json
+    from pathlib import Path
+    prof = Path(__file__).resolve().parents[1] / "profiles"
+    lines = [json.loads((prof / f).read_text()) for f in
+             ("r01_n1_bench.json", "r01_n2_bench.json", "r01_n4_bench.json")]
+    d = LayerCalibration()
+    one = LayerCalibration.from_bench(lines[0])           # slot wire, 1 GPU
+    assert abs(one.eff["dispatch_hbm"] - d.eff["dispatch_hbm"]) < 0.02
+    assert abs(one.eff["combine_hbm"] - d.eff["combine_hbm"]) < 0.02
+    c = LayerCalibration.from_bench(lines)
+    assert c.nvlink_gbs == 770.0 and c.hbm_gbs == d.hbm_gbs
+    assert abs(c.eff["pair_reduce"] - d.eff["pair_reduce"]) < 0.02     # 2 GPUs, HBM-bound
+    assert abs(c.eff["combine_nvlink"] - d.eff["combine_nvlink"]) < 0.02
+    assert abs(c.eff["pair_push_nvlink"] - d.eff["pair_push_nvlink"]) < 0.02
+    assert abs(c.gemm(768)[0] - d.gemm(768)[0]) < 0.02
+    assert abs(c.gemm(384)[0] - d.gemm(384)[0]) < 0.02
+    newer = LayerCalibration.from_bench(json.loads((prof / "r01b_n4_bench.json").read_text()), c)
+    assert newer.eff["pair_push_nvlink"] > c.eff["pair_push_nvlink"]   # bulk-copy pre-reduction
+    assert newer.eff["expand"] > 0.6
+    pred = predict_layer(_ids(0.0), 2, 2, E, H, I, newer)["seconds"] * 1e3
+    assert abs(pred - 0.332) / 0.332 < 0.15, pred
