@@ -209,6 +209,15 @@ MX_API int mx_stamp(mx_plan* p, int rank, int slot, void* stream);
 MX_API int mx_forward(mx_plan* p, int rank, const void* x, const float* logits,
                const int32_t* ids, const void* weights,
                const mx_expert_params* ep, void* y_out, void* stream);
+/* Error words of the last launches (the forward itself never syncs):
+ * synchronizes the stream, then reports and clears the rank's device error
+ * flags -- MX_ERR_CAPACITY "node d receives N routed slots, capacity C"
+ * (sim:346-351; rows past capacity are never written, the slot wire skips
+ * them and the token wire drops them from expand / pre-reduction),
+ * MX_ERR_INVALID for an expert id out of range, MX_ERR_TIMEOUT when a
+ * peer barrier's watchdog expired.  MoELayer.forward calls it after every
+ * eager forward; a captured forward checks with CapturedForward.check(). */
+MX_API int mx_plan_check(mx_plan* p, int rank, void* stream);
 
 /* ----- NCCL AR+A2A baseline helpers (value path of sim:598-680) -------
  * The baseline moves FULL-width rows with torch.distributed/NCCL

@@ -401,7 +401,7 @@ int mx_plan_buffer(mx_plan* p, int rank, int which, void** ptr, size_t* bytes) {
   const size_t elt = elt_bytes(d.act_dtype);
   size_t off = 0, len = 0;
   switch (which) {
-    case MX_BUF_RECV: off = o.recv; len = p->cap * h * elt; break;
+    case MX_BUF_RECV: off = o.recv; len = p->cap * (size_t)p->base.wrow; break;
     case MX_BUF_PARTIAL: off = o.partial; len = p->cap * h * elt; break;
     case MX_BUF_Y: off = o.y; len = T * h * elt; break;
     case MX_BUF_IDS: off = o.ids; len = 4 * T * k; break;
@@ -414,7 +414,7 @@ int mx_plan_buffer(mx_plan* p, int rank, int which, void** ptr, size_t* bytes) {
     case MX_BUF_SEND: off = o.send; len = 4 * n * n; break;
     case MX_BUF_ACT: off = o.act; len = p->cap * (size_t)p->base.I_t * 2; break;
     case MX_BUF_UPOS: off = o.upos; len = 4 * T * n; break;
-    case MX_BUF_XBUF: off = o.xbuf; len = (d.wire == MX_WIRE_TOKEN ? T * n : 0) * h * elt; break;
+    case MX_BUF_XBUF: off = o.xbuf; len = (d.wire == MX_WIRE_TOKEN ? T * n : 0) * (size_t)p->base.wrow; break;
     case MX_BUF_STAMPS: off = o.stamps; len = 8 * MX_STAMPS; break;
     default: set_error("bad buffer id %d", which); return MX_ERR_INVALID;
   }
@@ -467,22 +467,30 @@ int barrier(mx_plan* p, cudaStream_t s, bool group_only = false) {
   return launch_barrier(v, s, group_only);
 }
 
+// Reads (and clears) the rank's device error words: err[0] the largest host
+// row count over capacity (k_layout), err[1] an expert id out of range
+// (k_route), err[2] the barrier watchdog, err[3] a slot row past capacity.
+// Every word is cleared whichever fired, so a plan reused after an error
+// (simcluster caches plans) reports only its own later failures.
 int check_errors(mx_plan* p, int first, int last) {
   for (int r = first; r < last; ++r) {
     int err[4];
     MX_CUDA(cudaMemcpy(err, p->comm->heap[r] + p->off.err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (!(err[0] | err[1] | err[2] | err[3])) continue;
+    int rows[MX_NMAX] = {};
+    MX_CUDA(cudaMemcpy(rows, p->comm->heap[r] + p->off.host_rows, 4 * p->d.n_group, cudaMemcpyDeviceToHost));
+    const int zero[4] = {0, 0, 0, 0};
+    MX_CUDA(cudaMemcpy(p->comm->heap[r] + p->off.err, zero, sizeof(zero), cudaMemcpyHostToDevice));
     if (err[1]) { set_error("expert id out of range"); return MX_ERR_INVALID; }
-    if (err[0]) {
-      // report the first host over capacity with its slot count
-      int rows[MX_NMAX];
-      MX_CUDA(cudaMemcpy(rows, p->comm->heap[r] + p->off.host_rows, 4 * p->d.n_group, cudaMemcpyDeviceToHost));
+    if (err[0] || err[3]) {
+      // the first host over capacity with its slot count (sim:346-351)
       for (int d = 0; d < p->d.n_group; ++d)
         if (rows[d] > p->cap) {
           set_error("node %d receives %d routed slots, capacity %lld", d, rows[d], p->cap);
-          int zero[4] = {0, 0, 0, 0};
-          cudaMemcpy(p->comm->heap[r] + p->off.err, zero, sizeof(zero), cudaMemcpyHostToDevice);
           return MX_ERR_CAPACITY;
         }
+      set_error("routed slots exceed capacity %lld", p->cap);
+      return MX_ERR_CAPACITY;
     }
     if (err[2]) { set_error("peer barrier watchdog expired"); return MX_ERR_TIMEOUT; }
   }
@@ -779,6 +787,14 @@ int mx_baseline_combine_unpack(mx_plan* p, int rank, const void* recv, void* y, 
   if (it.last - it.first != 1) { set_error("baseline helpers take one rank"); return MX_ERR_INVALID; }
   return launch_baseline_combine_unpack(view_for(p, it.first), recv, y,
                                         static_cast<cudaStream_t>(stream));
+}
+
+int mx_plan_check(mx_plan* p, int rank, void* stream) {
+  RankIter it;
+  int rc = ranks_for(p, rank, &it);
+  if (rc) return rc;
+  MX_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return check_errors(p, it.first, it.last);
 }
 
 int mx_grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
       e = ids[si];
       w = wts[si];
       pos = slot_pos[si];
+      if (pos >= v.cap) { pos = 0; w = (A)0; }  // past capacity: never computed (mx_plan_check)
       const int d = home_of(e, n, E);
       key = (j - d - 1 + n) % n;  // arrival order (j-1, j-2, ..., j)
     }

@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(256) k_expand(DevView v) {
       for (int q = 0; q < 8; ++q)
         if (o + q * 512 < row_bytes) val[q] = ld_v4(src + o + q * 512);
       for (int i = 0; i < cnt; ++i) {
-        char* dst = recv + (size_t)__shfl_sync(0xffffffffu, row_l, i) * row_bytes + o;
+        const int row = __shfl_sync(0xffffffffu, row_l, i);
+        if (row >= v.cap) continue;  // flagged by the layout (mx_plan_check); never written
+        char* dst = recv + (size_t)row * row_bytes + o;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (o + q * 512 < row_bytes) st_v4(dst + q * 512, val[q]);
@@ -304,8 +306,9 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
 #pragma unroll
     for (int i = 0; i < KU; ++i) {
       const PairEnt<WT> e = pe[u * v.KH + (i < cnt ? i : 0)];
-      rp[i] = part + (size_t)e.p * h;
-      w[i] = (A)e.w;
+      const bool ok = e.p < v.cap;  // rows past capacity were never computed
+      rp[i] = part + (size_t)(ok ? e.p : 0) * h;
+      w[i] = ok ? (A)e.w : (A)0;
     }
     int c = lane * V;
     if (cnt <= KU) {
@@ -347,6 +350,7 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
       for (int q = 0; q < V; ++q) acc[q] = (A)0;
       for (int i = 0; i < cnt; ++i) {
         const PairEnt<WT> e = pe[u * v.KH + i];
+        if (e.p >= v.cap) continue;
         const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
         const T* pv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
@@ -463,8 +467,11 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
         if (b + pb >= u1) break;
         const int cnt = __shfl_sync(0xffffffffu, cnt_l, pb * 8);
         const int tok = __shfl_sync(0xffffffffu, tok_l, pb * 8);
-        const int ep = __shfl_sync(0xffffffffu, e.p, pb * 8 + j);
-        const float ew = __shfl_sync(0xffffffffu, e.w, pb * 8 + j);
+        const int ep_raw = __shfl_sync(0xffffffffu, e.p, pb * 8 + j);
+        const bool ok = ep_raw < v.cap;  // rows past capacity: weight 0, row 0 read
+        const int ep = ok ? ep_raw : 0;
+        const float ew_raw = __shfl_sync(0xffffffffu, e.w, pb * 8 + j);
+        const float ew = ok ? ew_raw : 0.f;
         const long long i = b + pb - u0;
         const int pi = (int)(i % PRB_NP);
         mbar_wait(&pempty[pi], (uint32_t)((i / PRB_NP) & 1) ^ 1u);
@@ -535,6 +542,7 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
           for (int q = 0; q < V; ++q) acc[q] = (A)0;
           for (int jj = 0; jj < cnt; ++jj) {
             const PairEnt<float> e = pe[(long long)u * v.KH + jj];
+            if (e.p >= v.cap) continue;
             const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
             const T* pv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
@@ -690,7 +698,7 @@ __global__ void k_rowsrc_token(DevView v) {
        q += (long long)gridDim.x * blockDim.x) {
     const long long u = q / v.KH;
     const int i = (int)(q % v.KH);
-    if (i < pn[u]) src[pe[q].p] = (int)u;
+    if (i < pn[u] && pe[q].p < v.cap) src[pe[q].p] = (int)u;
   }
 }
 

@@ -93,22 +93,37 @@ class MoELayer:
 
     # ------------------------------------------------------------ fused path
     def forward(self, x, logits=None, ids=None, weights=None, out=None,
-                stream=None):
+                stream=None, check=True):
         """Fused layer forward.  ``x``: [T, h] tokens of this rank's group
-        (device, or pinned host -> copied in); ``logits`` [T, E] f32 or
-        ``ids``/``weights`` [T, k].  Returns the [T, h] output (a view of the
-        layer's buffer, valid until the next call, or ``out`` when given --
-        a host ``out`` receives a device-to-host copy)."""
+        (device, or host -> copied in on ``stream``); ``logits`` [T, E] f32
+        or ``ids``/``weights`` [T, k].  Returns the [T, h] output (a view of
+        the layer's buffer, valid until the next call), or ``out`` when given
+        -- a host ``out`` is filled by a device-to-host copy on ``stream``
+        that has completed when this returns.
+
+        ``check`` (eager calls only; skipped while a CUDA graph captures)
+        synchronizes the stream and raises what the kernels flagged:
+        CapacityError when a host's routed slots exceed ``capacity``
+        (sim:346-351 -- the kernels never write past it), StrategyError for
+        an expert id out of range, NativeLibraryError when a peer barrier's
+        watchdog expired."""
         dev = self.plan.device
-        if not x.is_cuda:
-            x = x.to(dev, non_blocking=True)
-        if logits is not None and not logits.is_cuda:
-            logits = logits.to(dev, non_blocking=True)
-        self.plan.forward(x, self.params, logits=logits, ids=ids,
-                          weights=weights, rank=self.rank, stream=stream)
-        if out is None:
-            return self.y
-        out.copy_(self.y, non_blocking=True)
+        s = stream or torch.cuda.current_stream(dev)
+        with torch.cuda.stream(s):
+            if not x.is_cuda:
+                x = x.to(dev, non_blocking=True)
+            if logits is not None and not logits.is_cuda:
+                logits = logits.to(dev, non_blocking=True)
+            self.plan.forward(x, self.params, logits=logits, ids=ids,
+                              weights=weights, rank=self.rank, stream=s)
+            capturing = torch.cuda.is_current_stream_capturing()
+            if check and not capturing:
+                self.plan.check(rank=self.rank, stream=s)
+            if out is None:
+                return self.y
+            out.copy_(self.y, non_blocking=True)
+            if not out.is_cuda and not capturing:
+                s.synchronize()
         return out
 
     def forward_phases(self, x, logits, events, stream=None, event_factory=None):
@@ -288,6 +303,11 @@ class CapturedForward:
     def __call__(self):
         self.graph.replay()
         return self.layer.y
+
+    def check(self, stream=None):
+        """Synchronize and raise the errors the replays flagged (capacity,
+        expert ids, barrier watchdog); see :meth:`MoELayer.forward`."""
+        self.layer.plan.check(rank=self.layer.rank, stream=stream)
 
     def phase_ms(self):
         """(name, ms) per phase of the last replay (call after a sync)."""

@@ -182,8 +182,44 @@ class LayerPlan:
     def _r(self, rank):
         return -1 if rank is None else int(rank)
 
+    def _rows(self):
+        # emulated plans take every group's tokens stacked [n*T, ...]
+        return self.n * self.tokens if self.emulate else self.tokens
+
+    def _on_device(self, t, name, dtype, cols, convert):
+        """``t`` as a contiguous [rows, cols] ``dtype`` tensor on the plan's
+        device.  Routing tensors are converted (ids straight from
+        ``torch.topk`` are int64); the hidden states must already be the
+        plan's dtype.  Raises StrategyError like the reference's shape checks
+        (sim:341-344)."""
+        if not isinstance(t, torch.Tensor):
+            raise StrategyError(f"{name} must be a torch tensor, got {type(t).__name__}")
+        shape = (self._rows(), cols)
+        if tuple(t.shape) != shape:
+            raise StrategyError(f"{name} shape {tuple(t.shape)} mismatches {shape}")
+        if t.dtype != dtype:
+            if not convert:
+                raise StrategyError(f"{name} dtype {t.dtype} mismatches the plan's {dtype}")
+            t = t.to(dtype)
+        if t.device != self.device:
+            if t.is_cuda:
+                raise StrategyError(f"{name} lives on {t.device}, the plan on {self.device}")
+            t = t.to(self.device, non_blocking=True)
+        return t.contiguous()
+
+    def _routing_inputs(self, logits, ids, weights):
+        if (logits is None) == (ids is None):
+            raise StrategyError("pass exactly one of logits or ids")
+        if logits is not None:
+            return self._on_device(logits, "logits", torch.float32, self.num_experts, True), None, None
+        if weights is None:
+            raise StrategyError("ids need weights")
+        return (None, self._on_device(ids, "ids", torch.int32, self.top_k, True),
+                self._on_device(weights, "weights", self.wdtype, self.top_k, True))
+
     def route(self, logits=None, ids=None, weights=None, rank=None, stream=None):
         lib = N.load()
+        logits, ids, weights = self._routing_inputs(logits, ids, weights)
         N.check(lib.mx_route(self._plan, self._r(rank),
                              C.c_void_p(logits.data_ptr()) if logits is not None else None,
                              C.c_void_p(ids.data_ptr()) if ids is not None else None,
@@ -206,6 +242,7 @@ class LayerPlan:
         return self.buffer(rank, N.MX_BUF_STAMPS, torch.int64, (64,))
 
     def dispatch(self, x, rank=None, stream=None):
+        x = self._on_device(x, "x", self.dtype, self.hidden, False)
         N.check(N.load().mx_dispatch(self._plan, self._r(rank),
                                      C.c_void_p(x.data_ptr()), stream_ptr(stream)),
                 "dispatch")
@@ -221,6 +258,8 @@ class LayerPlan:
 
     def forward(self, x, params, logits=None, ids=None, weights=None,
                 y_out=None, rank=None, stream=None):
+        x = self._on_device(x, "x", self.dtype, self.hidden, False)
+        logits, ids, weights = self._routing_inputs(logits, ids, weights)
         N.check(N.load().mx_forward(
             self._plan, self._r(rank), C.c_void_p(x.data_ptr()),
             C.c_void_p(logits.data_ptr()) if logits is not None else None,
@@ -229,6 +268,14 @@ class LayerPlan:
             C.byref(params),
             C.c_void_p(y_out.data_ptr()) if y_out is not None else None,
             stream_ptr(stream)), "forward")
+
+    def check(self, rank=None, stream=None):
+        """Synchronize ``stream`` and raise the errors the device flagged
+        since the last check: CapacityError (a host's routed slots exceed
+        the capacity, sim:346-351), StrategyError (expert id out of range),
+        NativeLibraryError (peer barrier watchdog)."""
+        N.check(N.load().mx_plan_check(self._plan, self._r(rank), stream_ptr(stream)),
+                "forward")
 
     # ------------------------------------------------------------ views
     def rank_views(self, rank):

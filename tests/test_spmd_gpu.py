@@ -1,4 +1,13 @@
-"""Launch the SPMD parity check on every multi-GPU world the box offers."""
+"""Launch the SPMD parity check on every multi-GPU world the box offers, and
+on one GPU with every rank a separate process on cuda:0.
+
+The one-device form runs the real SPMD machinery -- per-process heaps
+exchanged as CUDA IPC handles, the system-scope flag barriers with their
+device epochs, graph capture and replay across processes -- on any box with
+one GPU (gloo bootstraps it; only the NCCL baseline arm is skipped).  The
+GPU time-slices the ranks' contexts, so each barrier waits for the other
+processes to be scheduled: slow, but exactly the cross-process ordering the
+multi-GPU layer depends on."""
 import os
 import subprocess
 import sys
@@ -11,16 +20,31 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _run(nproc, tp=None, env=None, port_off=0):
+def _run(nproc, tp=None, env=None, port_off=0, same_device=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
            f"--master-port={29500 + nproc * 7 + (tp or 0) + port_off}",
            str(ROOT / "tests" / "spmd_check.py")]
     if tp:
         cmd += ["--tp", str(tp)]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+    if same_device:
+        cmd += ["--same-device"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
                        env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "OK" in r.stdout, r.stdout[-4000:]
+    return r.stdout
+
+
+@pytest.mark.parametrize("nproc,tp", [(2, 1), (2, 2), (4, 2), (4, 4), (8, 2), (8, 4)])
+def test_spmd_layer_one_device(nproc, tp):
+    """nproc ranks as processes on cuda:0: IPC heaps, device barriers, graph
+    replay, f64 bit-exact / bf16 / fp8 parity, both wires (the 8-rank layouts
+    are config B's TP2 x EP4 and config C's TP4 x EP2)."""
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
+    out = _run(nproc, tp, port_off=100, same_device=True)
+    print(out[-2000:])
 
 
 @pytest.mark.parametrize("nproc,tp", [(2, 1), (2, 2), (4, 2), (4, 4), (8, 2), (8, 4)])
