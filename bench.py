@@ -133,22 +133,81 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU
+REF_DIR = ROOT / "oracle" / "_ref"   # the unmodified reference (oracle/install_ref.sh)
+
+
+def _import_reference():
+    """moeplan from oracle/_ref (pip-installed from /root/reference by
+    oracle/install_ref.sh; git-ignored, travels to the GPU box), or None."""
+    if not (REF_DIR / "moeplan" / "simcluster.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import moeplan.simcluster as sim
+    if not str(Path(sim.__file__).resolve()).startswith(str(REF_DIR.resolve())):
+        return None
+    return sim
+
+
+def reference_layer_step(sim, n, m, x, router, experts):
+    """One bounded sample of the layer through the reference's own stock
+    path: ``run_moe_block(mode="fused")`` (sim:565-595), f64, affine experts
+    (``ExpertSpec.default``), the whole n x m cluster simulated on the host."""
+    y, _trace = sim.run_moe_block(sim.build_cluster(n, m), x, router, experts, mode="fused")
+    return y
+
+
+def reference_inputs(sim, n, m, sample, seed=1):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((sample, H))
+    router = sim.RouterSpec.random(sample, E, K_TOP, seed=seed + 1)
+    return x, router, sim.ExpertSpec.default(E)
+
+
+def time_reference(n, m, sample, reps=None, target_s=10.0, warmup=1):
+    """Mean seconds per ``run_moe_block`` over a ``sample``-token batch of
+    the workload's shape (h, E, k, cluster n x m), on this host."""
+    sim = _import_reference()
+    if sim is None:
+        return None
+    x, router, ex = reference_inputs(sim, n, m, sample)
+    for _ in range(max(1, warmup)):
+        reference_layer_step(sim, n, m, x, router, ex)
+    if reps is None:
+        t0 = time.perf_counter()
+        reference_layer_step(sim, n, m, x, router, ex)
+        reps = max(3, int(np.ceil(target_s / max(time.perf_counter() - t0, 1e-3))))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        reference_layer_step(sim, n, m, x, router, ex)
+        times.append(time.perf_counter() - t0)
+    return float(np.mean(times)), reps
+
+
+def swiglu_port_experts(seed=0):
+    """SwiGLU expert weights for the CPU port, N(0, 1/fan_in) rounded to
+    bf16 (numpy only: the reference arm never imports the product)."""
+    from oracle import mixserve_oracle as orc
+    rng = np.random.default_rng(seed)
+    mk = lambda *s, fan: orc.bf16_round((rng.standard_normal(s, dtype=np.float32)
+                                         / np.float32(fan ** 0.5)))
+    return orc.SwiGLUOracle(mk(E, INTER, H, fan=H), mk(E, INTER, H, fan=H),
+                            mk(E, H, INTER, fan=INTER))
+
+
 def cpu_oracle_step(x, logits, experts_np):
-    """One bounded sample of the layer on the host: oracle gate + table +
-    batched SwiGLU experts (numpy/BLAS), expert-ascending accumulation."""
+    """One bounded sample of the SwiGLU layer on the host (the oracle port):
+    oracle gate + batched SwiGLU experts (numpy/BLAS), expert-ascending
+    accumulation."""
     from oracle import mixserve_oracle as orc
     ids, w = orc.router_topk(logits, K_TOP, renormalize=True)
     return orc.moe_layer_swiglu(x, ids, w, experts_np)
 
 
-def cpu_baseline(sample_tokens=512, reps=3, seed=0, target_s=10.0):
-    import torch
-    from paper_2601_08800_b200 import SwiGLUExperts
+def time_swiglu_port(sample_tokens=512, target_s=10.0, seed=0):
     from oracle import mixserve_oracle as orc
-    ex = SwiGLUExperts.random(E, H, INTER, seed=seed, device="cpu") \
-        if not torch.cuda.is_available() else SwiGLUExperts.random(E, H, INTER, seed=seed)
-    onp = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
-                           ex.w_down.float().cpu().numpy())
+    onp = swiglu_port_experts(seed)
     rng = np.random.default_rng(seed)
     x = orc.bf16_round(rng.standard_normal((sample_tokens, H)).astype(np.float32))
     logits = rng.standard_normal((sample_tokens, E)).astype(np.float32)
@@ -156,60 +215,81 @@ def cpu_baseline(sample_tokens=512, reps=3, seed=0, target_s=10.0):
     t0 = time.perf_counter()
     cpu_oracle_step(x, logits, onp)
     one = time.perf_counter() - t0
-    reps = max(reps, int(np.ceil(target_s / max(one, 1e-3))))  # ~target_s of CPU work
+    reps = max(3, int(np.ceil(target_s / max(one, 1e-3))))
     t0 = time.perf_counter()
     for _ in range(reps):
         cpu_oracle_step(x, logits, onp)
-    dt = (time.perf_counter() - t0) / reps
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": threads,
+    return (time.perf_counter() - t0) / reps, reps
+
+
+def cpu_threads():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def cpu_baseline(n, m, ref_sample=1024, port_sample=512, target_s=10.0):
+    """The reference's own CPU path (kind "reference": oracle/_ref's
+    run_moe_block, one core -- pure Python + elementwise numpy) on a bounded
+    sample of the workload, plus the SwiGLU port (numpy/BLAS, all host
+    threads) as a second, labelled line."""
+    port_dt, port_reps = time_swiglu_port(port_sample, target_s)
+    port = {"value": port_sample / port_dt, "unit": "tokens/s", "cores": cpu_threads(),
             "kind": "port",
-            "sample": f"{sample_tokens} tokens of the {T_GLOBAL}-token Qwen3-shape batch "
-                      f"(oracle gate + SwiGLU experts, f32 numpy/BLAS), mean of {reps} "
-                      f"repetitions (~{target_s:.0f} s of CPU work)",
-            "seconds_per_sample": dt}
+            "sample": f"{port_sample} tokens of the {T_GLOBAL}-token batch: oracle gate + "
+                      f"SwiGLU experts (f32 numpy/BLAS), mean of {port_reps} repetitions"}
+    ref = time_reference(n, m, ref_sample, target_s=target_s)
+    if ref is None:
+        port["note"] = "oracle/_ref missing (run oracle/install_ref.sh): the port is the baseline"
+        return port
+    dt, reps = ref
+    return {"value": ref_sample / dt, "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "sample": f"{ref_sample} tokens through the unmodified reference "
+                      f"run_moe_block(mode='fused') on a simulated {n}x{m} cluster (f64, "
+                      f"affine ExpertSpec.default({E}), RouterSpec.random top-{K_TOP}, "
+                      f"h={H}), mean of {reps} repetitions",
+            "seconds_per_sample": dt, "swiglu_port": port}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU implementation (oracle
-    port: the reference is pure Python and cannot travel to the GPU box),
-    rank 0 only, all host threads, bounded sample per step."""
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref: the unmodified moeplan, pip-installed from /root/reference
+    by oracle/install_ref.sh) through its public API, run_moe_block
+    (mode="fused"), f64 with its stock affine experts, on a bounded token
+    sample of this arm's workload (same h, E, k and n x m cluster layout).
+    Rank 0 only; the reference is single-threaded Python + numpy."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from paper_2601_08800_b200 import SwiGLUExperts
-    from oracle import mixserve_oracle as orc
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    ex = SwiGLUExperts.random(E, H, INTER, seed=0, device=dev)
-    onp = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
-                           ex.w_down.float().cpu().numpy())
-    del ex
+    n, m = reference_layout(args)
+    sim = _import_reference()
     sample = args.ref_sample
-    rng = np.random.default_rng(1)
-    x = orc.bf16_round(rng.standard_normal((sample, H)).astype(np.float32))
-    logits = rng.standard_normal((sample, E)).astype(np.float32)
-    for _ in range(max(1, min(args.warmup, 1))):
-        cpu_oracle_step(x, logits, onp)
+    if sim is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref missing: run oracle/install_ref.sh "
+                                         "(pip install --target oracle/_ref /root/reference)"}),
+              file=OUT, flush=True)
+        return
+    x, router, ex = reference_inputs(sim, n, m, sample)
+    for _ in range(max(1, min(args.warmup, 2))):
+        reference_layer_step(sim, n, m, x, router, ex)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        cpu_oracle_step(x, logits, onp)
+        reference_layer_step(sim, n, m, x, router, ex)
         times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     value = sample / dt
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     line = {
         "impl": "reference", "metric": "MoE-layer tokens/s", "value": value,
         "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "Qwen3-30B-A3B-shaped MoE layer, 8192-token prefill "
-                               f"(bounded sample of {sample} tokens per step)",
-                   "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"{sample} tokens per step, oracle port (numpy/BLAS)"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{WORKLOAD} (bounded sample of {sample} tokens per step)",
+                   "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP,
+                   "groups_n": n, "tp_m": m, "parallelism": f"TP{m}xEP{n}",
+                   "experts_kind": "reference ExpertSpec.default (affine, f64)"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                         "sample": f"{sample} tokens per step through the unmodified "
+                                   f"reference run_moe_block(mode='fused'), f64"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
