@@ -1,22 +1,32 @@
 #!/usr/bin/env python
 """MoE-layer tokens/s of the B200 TP-EP layer (BASELINE.json metric).
 
-Workload: BASELINE.json configs[1], the Qwen3-30B-A3B-shaped MoE layer
-(h=2048, moe_intermediate=768, 128 experts, top-8, bf16 SwiGLU experts,
-fp32 gate logits) on a prefill batch of 8192 tokens; one step = one full
-layer forward (gate top-k -> dispatch -> grouped GEMM -> combine) over the
-8192 tokens.  Total work is fixed as N grows ("scaling": "strong"); the
-cluster is TP2 x EP(N/2) (config B's TP2xEP4 at N=8), pure 1x1 at N=1.
+Workload (``--config``):
+  B (default) BASELINE.json configs[1], the Qwen3-30B-A3B-shaped MoE layer
+    (h=2048, moe_intermediate=768, 128 experts, top-8, bf16 SwiGLU experts,
+    fp32 gate logits), TP2 x EP(N/2) -- config B's TP2xEP4 at N=8;
+  C BASELINE.json configs[2], the DeepSeek-R1-shaped layer (h=7168,
+    I=2048, 256 routed experts top-8 + a 2048-wide shared expert, fp8 e4m3
+    experts, DeepSeek-V3 gate), TP4 x EP(N/4) -- TP4xEP2 at N=8.
+One step = one full layer forward (gate top-k -> dispatch -> grouped GEMM
+-> combine) over a prefill batch of 8192 tokens; total work is fixed as N
+grows ("scaling": "strong"); pure 1x1 at N=1.  ``--tp auto`` takes the
+fused-layer model's layout pick for the run's own routing.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--config B|C] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Timing: CUDA events on the launching stream around every step, L2 flushed
 (256 MiB write) between steps outside the events, max over ranks.  Per-
-phase events inside the same timed steps give the roofline of the dominant
-kernel.  ``e2e`` repeats the step through the public API with pinned host
-inputs and the output copied back.  The CPU baseline is the oracle port
-(oracle/, numpy + BLAS, all host threads) on a bounded token sample.
+phase events inside a second captured graph give each kernel's roofline
+(tensor phases against the burst bf16 peak -- they run inside a region of a
+few ms -- with the sustained figure beside it; NVLink phases against the
+same run's mx_nvlink_probe, 900 GB/s nominal beside it).  ``e2e`` streams
+pinned host inputs through the public API with the output copied back.  At
+N>1 the NCCL AR+A2A baseline is graph-captured the same way (static split
+sizes of this routing) and ``comm_us`` compares the two communicators.
+``cpu_baseline`` / ``--impl reference`` time the unmodified reference
+(oracle/_ref, run_moe_block) on a bounded token sample.
 """
 from __future__ import annotations
 
@@ -226,17 +236,21 @@ def cpu_threads():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
-def cpu_baseline(n, m, ref_sample=1024, port_sample=512, target_s=10.0):
+def cpu_baseline(n, m, ref_sample=1024, port_sample=512, target_s=10.0, with_port=True):
     """The reference's own CPU path (kind "reference": oracle/_ref's
     run_moe_block, one core -- pure Python + elementwise numpy) on a bounded
     sample of the workload, plus the SwiGLU port (numpy/BLAS, all host
     threads) as a second, labelled line."""
-    port_dt, port_reps = time_swiglu_port(port_sample, target_s)
-    port = {"value": port_sample / port_dt, "unit": "tokens/s", "cores": cpu_threads(),
-            "kind": "port",
-            "sample": f"{port_sample} tokens of the {T_GLOBAL}-token batch: oracle gate + "
-                      f"SwiGLU experts (f32 numpy/BLAS), mean of {port_reps} repetitions"}
+    port = None
+    if with_port:
+        port_dt, port_reps = time_swiglu_port(port_sample, target_s)
+        port = {"value": port_sample / port_dt, "unit": "tokens/s", "cores": cpu_threads(),
+                "kind": "port",
+                "sample": f"{port_sample} tokens of the {T_GLOBAL}-token batch: oracle gate + "
+                          f"SwiGLU experts (f32 numpy/BLAS), mean of {port_reps} repetitions"}
     ref = time_reference(n, m, ref_sample, target_s=target_s)
+    if ref is None and port is None:
+        return None
     if ref is None:
         port["note"] = "oracle/_ref missing (run oracle/install_ref.sh): the port is the baseline"
         return port
@@ -297,30 +311,32 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours
-def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
+def phase_model(S, n, m, group, T, U=None, wire="slot"):
     """Algorithmic bytes / flops per launch of every phase on this rank
     (SURVEY.md §8(d)); S[j][d] = slots of group j hosted on group d,
-    U[j][d] = tokens of group j hitting host d (wire TOKEN)."""
+    U[j][d] = tokens of group j hitting host d (wire TOKEN).  Wire rows are
+    WROW bytes (bf16: 2h; fp8: h e4m3 + 16 B scale tail), partials / ZIN /
+    y rows 2h bytes (bf16)."""
     It = INTER // m
+    Ist = SHARED // m
     S_d = int(S[:, group].sum())             # rows this rank's GEMMs process
     remote_in = int(S[:, group].sum() - S[group, group])   # rows received over NVLink
     local_rows = int(S[group, group])
-    hb = H * 2
+    hb = WROW                                # a token row on the wire
+    ob = H * 2                               # a partial / output row
     slots = T * K_TOP
     model = {}
     model["route"] = {"bound": "hbm", "bytes": T * E * 4 + slots * 16 + E * 4}
     if n * m == 1:
         # x read once (slot rows re-read from L2), expert-major rows written
-        model["dispatch"] = {"bound": "hbm", "bytes": T * hb + S_d * hb}
-        model["combine"] = {"bound": "hbm", "bytes": slots * hb + T * hb}
+        model["dispatch"] = {"bound": "hbm", "bytes": T * H * 2 + S_d * hb}
+        model["combine"] = {"bound": "hbm", "bytes": slots * ob + T * ob}
     else:
         if remote_in > 0:
             model["dispatch"] = {"bound": "nvlink", "bytes": remote_in * hb,
                                  "local_hbm_bytes": 2 * local_rows * hb}
         else:   # one group (pure TP): every row is a local gather
             model["dispatch"] = {"bound": "hbm", "bytes": T * hb + S_d * hb}
-        # pulls: every slot's column shard from the m TP ranks of its host,
-        # minus the one local read; plus the (m-1)/m of y pushed by TP peers
         own_host_slots = int(S[group, group])
         remote_pull = (slots * m - own_host_slots) * (H // m) * 2
         model["combine"] = {"bound": "nvlink",
@@ -343,20 +359,20 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
         # the owners' ZIN: all of it crosses NVLink for other groups' tokens,
         # (m-1)/m of it for the own group's; it reads S_d partial rows locally
         own = int(U[group, group])
-        push = (pairs_host - own) * hb + own * hb * (m - 1) // m
+        push = (pairs_host - own) * ob + own * ob * (m - 1) // m
         if push > 0:
             model["pair_reduce"] = {"bound": "nvlink", "bytes": push,
-                                    "local_hbm_bytes": S_d * hb}
+                                    "local_hbm_bytes": S_d * ob}
         else:
-            model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * hb + pairs_host * hb}
+            model["pair_reduce"] = {"bound": "hbm", "bytes": S_d * ob + pairs_host * ob}
         # the owner sums its local ZIN planes and pushes its y shard to the
         # group's other TP ranks (final all-gather)
-        zin_read = int(U[group].sum()) * hb
+        zin_read = int(U[group].sum()) * ob
         y_push = T * H * (m - 1) // m * 2
         if y_push > 0:
             model["combine"] = {"bound": "nvlink", "bytes": y_push, "local_hbm_bytes": zin_read}
         else:
-            model["combine"] = {"bound": "hbm", "bytes": zin_read + T * hb}
+            model["combine"] = {"bound": "hbm", "bytes": zin_read + T * ob}
     # a phase that moves both NVLink and local HBM bytes is judged against
     # whichever of the two takes longer at its peak
     for spec in model.values():
@@ -367,9 +383,133 @@ def phase_model(S, cnt, n, m, group, tp, T, U=None, wire="slot"):
             spec["bound"], spec["bytes"] = "hbm", loc
         elif loc is not None:
             spec["local_hbm_bytes"] = loc
-    model["gemm1_swiglu"] = {"bound": "tensor", "flops": 2 * S_d * H * 2 * It}
-    model["gemm2"] = {"bound": "tensor", "flops": 2 * S_d * It * H}
+    # stage 1 = routed GEMM1 (+ the shared expert's GEMM1), stage 2 = GEMM2s
+    model["gemm1_swiglu"] = {"bound": "tensor",
+                             "flops": 2 * S_d * H * 2 * It + 2 * T * H * 2 * Ist}
+    model["gemm2"] = {"bound": "tensor", "flops": 2 * S_d * It * H + 2 * T * Ist * H}
     return model
+
+
+def measure_fp8_peak(dev):
+    """Dense e4m3 matmul peak on this GPU, the MEASURED_PEAKS method for
+    bf16 applied to fp8: torch._scaled_mm 8192^3 (cuBLASLt), best of 10,
+    CUDA events (TFLOP/s)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, device=dev).to(torch.float8_e4m3fn)
+    b = torch.randn(n, n, device=dev).to(torch.float8_e4m3fn).t()
+    one = torch.ones((), device=dev)
+    for _ in range(3):
+        torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+    best = 1e9
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best / 1e3) / 1e12
+
+
+def nvlink_probe(layer, world, reps=5, mb_per_peer=32):
+    """Same-run NVLink denominator: every rank copies ``mb_per_peer`` MB
+    to every peer at once through the layer's own IPC heaps (16 B loads +
+    16 B stores, mx_nvlink_probe); per-GPU egress GB/s, the slowest rank of
+    the best of ``reps`` timed launches."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_08800_b200 import _native as N
+    from paper_2601_08800_b200.plan import stream_ptr
+    p = layer.plan
+    recv_room = p.buffer_bytes(layer.rank, N.MX_BUF_RECV) // world
+    part_room = p.buffer_bytes(layer.rank, N.MX_BUF_PARTIAL)
+    per_peer = min(mb_per_peer << 20, recv_room, part_room) & ~4095
+    s = torch.cuda.current_stream()
+    best = None
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        dist.barrier()
+        p.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        N.check(N.load().mx_nvlink_probe(p._plan, per_peer, stream_ptr(s)), "probe")
+        b.record(s)
+        torch.cuda.synchronize()
+        ms = torch.tensor([a.elapsed_time(b)], device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        t = float(ms.item())
+        best = t if best is None else min(best, t)
+    gbs = per_peer * (world - 1) / (best / 1e3) / 1e9
+    return {"gbs_per_gpu": gbs, "bytes_per_peer": per_peer, "ms": best,
+            "how": "mx_nvlink_probe: every rank copies bytes_per_peer of local HBM to every "
+                   "peer's heap at once (16 B loads, 16 B NVLink stores), best of "
+                   f"{reps}, slowest rank"}
+
+
+def timed_replays(run, steps, flush, plan_barrier, stream, world):
+    """Sum of per-step CUDA-event times of ``run()`` over ``steps`` replays
+    (L2 flushed and ranks aligned before each), max over ranks (ms)."""
+    import torch
+    import torch.distributed as dist
+    ev = []
+    for _ in range(steps):
+        flush.fill_(1)
+        plan_barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run()
+        b.record(stream)
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    t = torch.tensor([float(sum(a.elapsed_time(b) for a, b in ev))], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def phase_avgs(runner, steps, flush, plan_barrier):
+    import torch
+    times = {}
+    for _ in range(steps):
+        flush.fill_(1)
+        plan_barrier()
+        runner()
+        torch.cuda.synchronize()
+        for name, ms in runner.phase_ms():
+            times.setdefault(name, []).append(ms)
+    return {k: float(np.mean(v)) for k, v in times.items()}
+
+
+FUSED_COMM = ("barrier_counts", "dispatch", "barrier_dispatch", "expand", "pair_reduce",
+              "barrier_partials", "combine", "barrier_out")
+NCCL_COMM = ("a2a_dispatch", "a2a_combine", "allreduce")
+
+
+def build_layer(args, world, rank, n, m, wire, T):
+    """The MoE layer of the selected config with random-init weights."""
+    import torch
+    from paper_2601_08800_b200 import FP8SwiGLUExperts, SwiGLUExperts
+    from paper_2601_08800_b200.layer import MoELayer
+    from paper_2601_08800_b200.plan import GateSpec
+    if CONFIG == "C":
+        ex = FP8SwiGLUExperts.random(E, H, INTER, shared_inter=SHARED, seed=0)
+        ex.rank_shard(n, m, rank)                     # cached e4m3 shard of this rank
+        ex.src = ex.shared = None                     # free the bf16 sources
+        torch.cuda.empty_cache()
+        bias = (0.05 * torch.randn(E, generator=torch.Generator().manual_seed(3))).float()
+        gate = GateSpec.deepseek_v3(bias, groups=8, topk_groups=4, scaling=2.5)
+        layer = MoELayer(n, m, T, H, E, K_TOP, INTER, experts=ex, rank=rank, wire=wire,
+                         gate=gate)
+        return layer, None
+    ex = SwiGLUExperts.random(E, H, INTER, seed=0)
+    w13, w2 = ex.rank_shard(n, m, rank)
+    del ex
+    torch.cuda.empty_cache()
+    layer = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank, wire=wire)
+    return layer, (w13, w2)
 
 
 def run_ours(args):
@@ -384,25 +524,20 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2601_08800_b200 import SwiGLUExperts
     from paper_2601_08800_b200.layer import MoELayer, layout_for
 
-    n, m = layout_for(world, args.tp)
+    n, m = choose_layout(args, world)
     group, tp = divmod(rank, m)
     T = T_GLOBAL // n
-    ex = SwiGLUExperts.random(E, H, INTER, seed=0)
-    w13, w2 = ex.rank_shard(n, m, rank)
-    del ex
-    torch.cuda.empty_cache()
     # TOKEN wire whenever there is a peer: dedup dispatch + pair pre-reduction
-    # (for n == 1 the TP reduction then moves T rows instead of T*k slots)
     wire = args.wire if args.wire != "auto" else ("token" if world > 1 else "slot")
-    layer = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank, wire=wire)
+    layer, weights = build_layer(args, world, rank, n, m, wire, T)
     g = torch.Generator(device="cuda").manual_seed(1000 + group)
     x = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
     logits = torch.randn(T, E, device="cuda", generator=g)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    barrier = layer.plan.barrier
 
     def sync_all():
         torch.cuda.synchronize()
@@ -410,37 +545,22 @@ def run_ours(args):
             dist.barrier()
 
     for _ in range(args.warmup):
-        layer.forward(x, logits)
+        layer.forward(x, logits)                  # eager, error-checked
     sync_all()
     S = layer.routing_counts()[1].astype(np.int64)
-    cnt = layer.routing_counts()[0]
     U = layer.pair_counts()
 
     # ---- timed region: K replays of the captured layer forward (one CUDA
     #      graph: every launch and device barrier), CUDA events around each
     #      replay on the launching stream, L2 flushed between steps
     runner = layer.capture(x, logits)
-    step_ev = []
     with ClockSampler(local) as clk:
         clk.wait_first()
         sync_all()
         t_region0 = time.monotonic()
-        for _ in range(args.steps):
-            flush.fill_(1)
-            layer.plan.barrier()   # align ranks before the start event (launch skew)
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            runner()
-            b.record(stream)
-            step_ev.append((a, b))
-        torch.cuda.synchronize()
+        total_ms = timed_replays(runner, args.steps, flush, barrier, stream, world)
         t_region1 = time.monotonic()
-    total_ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
-    t = torch.tensor([total_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    runner.check()                                # errors flagged during the replays
     ms_per_step = total_ms / args.steps
     value = T_GLOBAL / (ms_per_step / 1e3)
 
@@ -448,21 +568,184 @@ def run_ours(args):
     #      event after every phase (each event node adds ~3 us, so this loop
     #      is reported apart from the headline), K replays, L2 flushed
     phased = layer.capture(x, logits, with_events=True)
-    phase_times = {}
-    for _ in range(args.steps):
-        flush.fill_(1)
-        layer.plan.barrier()
-        phased()
-        torch.cuda.synchronize()
-        for name, ms in phased.phase_ms():
-            phase_times.setdefault(name, []).append(ms)
+    avg = phase_avgs(phased, args.steps, flush, barrier)
+    del phased
 
-    # ---- e2e through the public API, streamed the way a server feeds
-    #      batches: every step copies its tokens/logits in from pinned host
-    #      memory and its output back out; the H2D of step i+1 and the D2H of
-    #      step i run on their own streams under the forward of step i
-    #      (double-buffered inputs, two captured graphs).  One timed region
-    #      over the K steps, max over ranks.
+    # ---- e2e through the public API (see run_e2e)
+    e2e = run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync_all)
+    del runner
+
+    extras = {}
+    nvl = None
+    if world > 1:
+        nvl = nvlink_probe(layer, world)
+        extras["nvlink_probe"] = nvl
+    nvl_peak = nvl["gbs_per_gpu"] if nvl else NVLINK_PEER_GBS
+
+    # ---- NCCL AR + A2A baseline, graph-captured with this routing's split
+    #      sizes fixed (no host sync inside), same timing loop; per-phase
+    #      events give the communicator-only comparison
+    if world > 1 and not args.no_nccl:
+        bl = layer.capture_baseline(x, logits)
+        bl_ms = timed_replays(bl, args.steps, flush, barrier, stream, world) / args.steps
+        blp = layer.capture_baseline(x, logits, with_events=True)
+        bl_avg = phase_avgs(blp, args.steps, flush, barrier)
+        del blp
+        nccl = {"ms_per_step": bl_ms, "tokens_per_s": T_GLOBAL / (bl_ms / 1e3),
+                "layout": "NCCL all_to_all_single x2 (full width, every TP rank) + TP all_reduce",
+                "captured": bl.graph is not None,
+                "split_sizes": "this routing's send matrix, read once before capture (static)",
+                "fused_speedup": bl_ms / ms_per_step, "phases_us": {k: v * 1e3 for k, v in bl_avg.items()}}
+        if bl.error:
+            nccl["capture_error"] = bl.error
+        del bl
+        extras["nccl_baseline"] = nccl
+        fused_comm = sum(avg.get(k, 0.0) for k in FUSED_COMM) * 1e3
+        nccl_comm = sum(bl_avg.get(k, 0.0) for k in NCCL_COMM) * 1e3
+        extras["comm_us"] = {
+            "fused": fused_comm, "nccl": nccl_comm,
+            "fused_phases": [k for k in FUSED_COMM if k in avg],
+            "nccl_phases": list(NCCL_COMM),
+            "speedup": nccl_comm / fused_comm if fused_comm else None,
+            "overlap_with_expert_gemms": "none: fused phases are serialized with the GEMMs",
+            "note": "fused: dispatch/expand/pair pre-reduction (RS fused)/combine (AG fused) + "
+                    "device barriers; NCCL: pack + all_to_all (dispatch), pack + all_to_all "
+                    "(combine), unpack + TP all_reduce; per-phase events, L2 flushed"}
+
+    # ---- the reference's per-slot wire, and EP-only, on the same GPUs
+    if world > 1 and wire == "token" and not args.no_nccl and CONFIG == "B":
+        alt = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=weights[0], w2=weights[1], rank=rank,
+                       wire="slot")
+        ms = timed_replays(alt.capture(x, logits), args.steps, flush, alt.plan.barrier,
+                           stream, world) / args.steps
+        extras["wire_slot"] = {"ms_per_step": ms, "tokens_per_s": T_GLOBAL / (ms / 1e3),
+                               "wire": "slot (the reference's one-row-per-slot A2A layout)"}
+        alt.close()
+    if world > 1 and m > 1 and not args.no_nccl and CONFIG == "B":
+        from paper_2601_08800_b200 import SwiGLUExperts
+        xe_g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        Te = T_GLOBAL // world
+        xe = torch.randn(Te, H, device="cuda", generator=xe_g).to(torch.bfloat16)
+        le = torch.randn(Te, E, device="cuda", generator=xe_g)
+        ex2 = SwiGLUExperts.random(E, H, INTER, seed=0)
+        w13e, w2e = ex2.rank_shard(world, 1, rank)
+        del ex2
+        alt = MoELayer(world, 1, Te, H, E, K_TOP, INTER, w13=w13e, w2=w2e, rank=rank,
+                       wire="token")
+        ms = timed_replays(alt.capture(xe, le), args.steps, flush, alt.plan.barrier,
+                           stream, world) / args.steps
+        extras["layout_ep_only"] = {"parallelism": f"TP1xEP{world}", "wire": "token",
+                                    "ms_per_step": ms, "tokens_per_s": T_GLOBAL / (ms / 1e3)}
+        alt.close()
+        del w13e, w2e, xe, le
+        torch.cuda.empty_cache()
+
+    # ---- roofline of every phase (this rank; rank 0 reports) and of the
+    #      dominant kernel
+    pk, pk_kind = peaks()
+    if CONFIG == "C":
+        tensor_peak = measure_fp8_peak("cuda")
+        tensor_peak_src = ("measured in-run: torch._scaled_mm e4m3 8192^3, best of 10 "
+                           "(cuBLASLt, the MEASURED_PEAKS bf16 method)")
+        tensor_sus, tensor_sus_src = None, None
+    else:
+        tensor_peak = pk["bf16_tflops"]
+        tensor_peak_src = (f"{pk_kind} bf16 burst (best-of-10 8192^3 matmul): the kernels "
+                           f"are timed inside a {total_ms:.0f} ms region")
+        tensor_sus = pk.get("bf16_tflops_sustained")
+        tensor_sus_src = f"{pk_kind} bf16 sustained (4 s back-to-back)"
+    model = phase_model(S, n, m, group, T, U, wire)
+    rooflines = {}
+    for ph, spec in model.items():
+        if ph not in avg or avg[ph] <= 0 or spec.get("bytes", 1) == 0:
+            continue
+        sec = avg[ph] / 1e3
+        r = {"bound": spec["bound"], "us": avg[ph] * 1e3}
+        if spec["bound"] == "tensor":
+            r.update(achieved=spec["flops"] / sec / 1e12, peak=tensor_peak, unit="TFLOP/s",
+                     peak_source=tensor_peak_src)
+            if tensor_sus:
+                r.update(peak_sustained=tensor_sus, frac_sustained=r["achieved"] / tensor_sus)
+        elif spec["bound"] == "hbm":
+            r.update(achieved=spec["bytes"] / sec / 1e9, peak=pk["hbm_gbs"], unit="GB/s",
+                     peak_source=f"{pk_kind} HBM copy")
+        else:
+            r.update(achieved=spec["bytes"] / sec / 1e9, peak=nvl_peak, unit="GB/s",
+                     peak_source=("same-run mx_nvlink_probe (SM-issued peer copies, all "
+                                  "peers at once)") if nvl else "NVLink peer copy 770 GB/s",
+                     nominal=900.0, frac_nominal=spec["bytes"] / sec / 1e9 / 900.0)
+        r["frac"] = r["achieved"] / r["peak"]
+        rooflines[ph] = r
+    dom = max(rooflines, key=lambda k: rooflines[k]["us"]) if rooflines else None
+    roof = dict(rooflines[dom]) if dom else None
+    if roof is not None:
+        roof["kernel"] = dom
+        traffic = None
+        tp_file = ROOT / "profiles" / "traffic.json"
+        if tp_file.exists():
+            traffic = json.loads(tp_file.read_text()).get(f"{CONFIG}{world}", {}).get(dom)
+        roof["traffic"] = traffic
+        roof["traffic_source"] = ("ncu --set full capture of this kernel at this config "
+                                  "(profiles/traffic.json), not measured in this run"
+                                  if traffic is not None else None)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(n, m, ref_sample=args.ref_sample if CONFIG == "B" else 256,
+                           port_sample=args.cpu_sample, with_port=CONFIG == "B")
+
+    if rank == 0:
+        line = {
+            "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp8" if CONFIG == "C" else "bf16",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "config": CONFIG,
+                       "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP,
+                       "shared_intermediate": SHARED, "global_tokens": T_GLOBAL,
+                       "groups_n": n, "tp_m": m, "parallelism": f"TP{m}xEP{n}",
+                       "layout_choice": LAYOUT_NOTE,
+                       "l2": "flushed (256 MiB write) between steps", "wire": wire,
+                       "weights": "random init, seed 0"},
+            "clocks": clk.summary(t_region0, t_region1),
+            "e2e": e2e,
+            "gpu_launches": launches_per_step(world, m, wire) * args.steps,
+            "roofline": roof,
+            "rooflines": rooflines,
+            "phases_us": {k: v * 1e3 for k, v in avg.items()},
+            "phases_note": "per-phase CUDA events inside a second captured graph, same K, "
+                           "L2 flushed; each event node adds ~3 us",
+            "cpu_baseline": cpu,
+        }
+        line.update(extras)
+        print(json.dumps(line), file=OUT, flush=True)
+    layer.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def launches_per_step(world, m, wire):
+    """Kernels of one captured forward (profiles/r01_n1_launches.csv):
+    gate, route, scan, layout, dispatch, gemm1, gemm2, combine; + barriers
+    (3, +1 TP-group barrier when m > 1) with peers; + expand, pair_reduce on
+    the token wire; config C adds the token quantisation, the activation
+    re-quantisation and the shared expert's two GEMMs + quantisation."""
+    k = 8 + ((4 if m > 1 else 3) if world > 1 else 0) + (2 if wire == "token" else 0)
+    if CONFIG == "C":
+        k += 5
+    return k
+
+
+def run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync_all):
+    """e2e through the public API, streamed the way a server feeds batches:
+    every step copies its tokens/logits in from pinned host memory and its
+    output back out; the H2D of step i+1 and the D2H of step i run on their
+    own streams under the forward of step i (double-buffered inputs, two
+    captured graphs).  One timed region over the K steps, max over ranks."""
+    import torch
+    import torch.distributed as dist
     x_h = x.cpu().pin_memory()
     l_h = logits.cpu().pin_memory()
     y_hs = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
@@ -517,180 +800,80 @@ def run_ours(args):
     t = torch.tensor([e_a.elapsed_time(e_b)], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    runners[1].check()
     e2e_step = float(t.item()) / args.steps
-    x_h_bytes = x_h.numel() * 2
-    del runners
-    h2d = (x_h_bytes + l_h.numel() * 4) * world
+    h2d = (x_h.numel() * 2 + l_h.numel() * 4) * world
     d2h = T * H * 2 * n
+    return {"value": T_GLOBAL / (e2e_step / 1e3), "unit": "tokens/s",
+            "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h),
+            "note": "every step: pinned host x/logits copied in (H2D stream), the captured "
+                    "MoELayer forward, y copied back to pinned host (D2H stream); copies of "
+                    "neighbouring steps overlap the forward (double-buffered); one timed "
+                    "region over all steps"}
 
-    # ---- the reference's per-slot wire on the same config (N > 1)
-    slot_wire = None
-    if world > 1 and wire == "token" and not args.no_nccl:
-        alt = MoELayer(n, m, T, H, E, K_TOP, INTER, w13=w13, w2=w2, rank=rank, wire="slot")
-        alt_run = alt.capture(x, logits)
-        ev = []
-        for _ in range(args.steps):
-            flush.fill_(1)
-            alt.plan.barrier()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            alt_run()
-            b.record(stream)
-            ev.append((a, b))
-        torch.cuda.synchronize()
-        st = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device="cuda")
-        dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        slot_wire = {"ms_per_step": float(st.item()),
-                     "tokens_per_s": T_GLOBAL / (float(st.item()) / 1e3),
-                     "wire": "slot (the reference's one-row-per-slot A2A layout)"}
-        del alt_run
-        alt.close()
 
-    # ---- the other layout of the same GPUs: EP only (TP1 x EP N) -- the
-    #      layout the strategy question is about (config E / SURVEY §8 a15)
-    ep_only = None
-    if world > 1 and m > 1 and not args.no_nccl:
-        xe_g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-        Te = T_GLOBAL // world
-        xe = torch.randn(Te, H, device="cuda", generator=xe_g).to(torch.bfloat16)
-        le = torch.randn(Te, E, device="cuda", generator=xe_g)
-        ex2 = SwiGLUExperts.random(E, H, INTER, seed=0)
-        w13e, w2e = ex2.rank_shard(world, 1, rank)
-        del ex2
-        alt = MoELayer(world, 1, Te, H, E, K_TOP, INTER, w13=w13e, w2=w2e, rank=rank, wire="token")
-        alt_run = alt.capture(xe, le)
-        ev = []
-        for _ in range(args.steps):
-            flush.fill_(1)
-            alt.plan.barrier()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            alt_run()
-            b.record(stream)
-            ev.append((a, b))
-        torch.cuda.synchronize()
-        st = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], device="cuda")
-        dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        ep_only = {"parallelism": f"TP1xEP{world}", "wire": "token",
-                   "ms_per_step": float(st.item()),
-                   "tokens_per_s": T_GLOBAL / (float(st.item()) / 1e3)}
-        del alt_run
-        alt.close()
-        del w13e, w2e, xe, le
-        torch.cuda.empty_cache()
+LAYOUT_NOTE = ""
 
-    # ---- NCCL AR + A2A baseline on the same config (N > 1)
-    nccl = None
-    if world > 1 and not args.no_nccl:
-        for _ in range(2):
-            layer.forward_baseline(x, logits)
-        sync_all()
-        bl = []
-        for _ in range(max(3, args.steps // 2)):
-            flush.fill_(1)
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            layer.forward_baseline(x, logits)
-            b.record(stream)
-            bl.append((a, b))
-        torch.cuda.synchronize()
-        blt = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in bl]))], device="cuda")
-        dist.all_reduce(blt, op=dist.ReduceOp.MAX)
-        nccl = {"ms_per_step": float(blt.item()),
-                "tokens_per_s": T_GLOBAL / (float(blt.item()) / 1e3),
-                "layout": "NCCL all_to_all_single x2 (full width, every TP rank) + TP all_reduce",
-                "fused_speedup": float(blt.item()) / ms_per_step}
 
-    # ---- roofline of the dominant kernel (this rank; rank 0 reports)
-    pk, pk_kind = peaks()
-    model = phase_model(S, cnt, n, m, group, tp, T, U, wire)
-    avg = {k: float(np.mean(v)) for k, v in phase_times.items()}
-    rooflines = {}
-    for ph, spec in model.items():
-        if ph not in avg or avg[ph] <= 0 or spec.get("bytes", 1) == 0:
-            continue
-        sec = avg[ph] / 1e3
-        if spec["bound"] == "tensor":
-            ach = spec["flops"] / sec / 1e12
-            peak, unit = pk["bf16_tflops_sustained"], "TFLOP/s"
-            peak_src = f"{pk_kind} bf16 sustained"
-        elif spec["bound"] == "hbm":
-            ach = spec["bytes"] / sec / 1e9
-            peak, unit = pk["hbm_gbs"], "GB/s"
-            peak_src = f"{pk_kind} HBM copy"
-        else:
-            ach = spec["bytes"] / sec / 1e9
-            peak, unit = NVLINK_PEER_GBS, "GB/s"
-            peak_src = "NVLink peer copy 770 GB/s/direction (B200_PROFILING.md)"
-        rooflines[ph] = {"bound": spec["bound"], "achieved": ach, "peak": peak, "unit": unit,
-                         "frac": ach / peak, "us": avg[ph] * 1e3, "peak_source": peak_src}
-        if spec["bound"] == "nvlink":
-            rooflines[ph]["frac_sm_store_ceiling"] = ach / NVLINK_SM_STORE_GBS
-            rooflines[ph]["sm_store_ceiling_source"] = (
-                f"{NVLINK_SM_STORE_GBS:.0f} GB/s, profiles/r01_nvlink_ceiling_n4.jsonl")
-    kernels = {k: v for k, v in rooflines.items()}
-    dom = max(kernels, key=lambda k: kernels[k]["us"]) if kernels else None
-    traffic = None
-    tp_file = ROOT / "profiles" / "traffic.json"
-    if dom and tp_file.exists():
-        traffic = json.loads(tp_file.read_text()).get(f"n{world}", {}).get(dom)
-    roof = dict(kernels[dom]) if dom else None
-    if roof is not None:
-        roof["kernel"] = dom
-        roof["traffic"] = traffic
+def choose_layout(args, world):
+    """(n, m) of the run: the config's named layout (B: TP2 x EP(N/2), C:
+    TP4 x EP(N/4), pure TP/EP below that), an explicit --tp, or --tp auto:
+    the fused-layer model's first pick (layer_model.select_layout) for this
+    run's own routing (every rank computes it from the same seeded logits)."""
+    global LAYOUT_NOTE
+    from paper_2601_08800_b200.layer import layout_for
+    if args.tp == "auto" and world > 1:
+        import torch
+        logits = torch.cat([torch.randn(T_GLOBAL // world, E, device="cuda",
+                                        generator=torch.Generator(device="cuda").manual_seed(
+                                            2000 + r)) for r in range(world)])
+        ids = torch.topk(logits, K_TOP, dim=-1).indices.cpu().numpy()
+        n, m = layout_for(world, "auto", routing=ids, num_experts=E, hidden=H, inter=INTER)
+        LAYOUT_NOTE = "auto: layer_model.select_layout on a routing sample of this workload"
+        return n, m
+    if args.tp not in (None, "auto"):
+        LAYOUT_NOTE = "--tp"
+        return layout_for(world, int(args.tp))
+    tp = 1 if world == 1 else min(world, 4 if CONFIG == "C" else 2)
+    LAYOUT_NOTE = f"config {CONFIG}'s named layout (TP{tp} x EP{world // tp})"
+    return layout_for(world, tp)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(sample_tokens=args.cpu_sample)
 
-    # gate, route, scan, layout, dispatch, gemm1, gemm2, combine (+3 barriers,
-    # +1 TP-group barrier when m > 1; +expand, +pair_reduce for wire TOKEN)
-    # -- profiles/r01_n1_launches.csv
-    launches_per_step = (8 + ((4 if m > 1 else 3) if world > 1 else 0)
-                         + (2 if wire == "token" else 0))
-    if rank == 0:
-        line = {
-            "metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "Qwen3-30B-A3B-shaped MoE layer (BASELINE configs[1]), "
-                                   "8192-token prefill, bf16 SwiGLU experts, fp32 gate logits",
-                       "hidden": H, "moe_intermediate": INTER, "experts": E, "top_k": K_TOP,
-                       "global_tokens": T_GLOBAL, "groups_n": n, "tp_m": m,
-                       "parallelism": f"TP{m}xEP{n}", "l2": "flushed (256 MiB write) between steps",
-                       "wire": wire,
-                       "weights": "random init, seed 0"},
-            "clocks": clk.summary(t_region0, t_region1),
-            "e2e": {"value": T_GLOBAL / (e2e_step / 1e3), "unit": "tokens/s",
-                    "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h),
-                    "note": "every step: pinned host x/logits copied in (H2D stream), the "
-                            "captured MoELayer forward, y copied back to pinned host (D2H "
-                            "stream); copies of neighbouring steps overlap the forward "
-                            "(double-buffered); one timed region over all steps"},
-            "gpu_launches": launches_per_step * args.steps,
-            "roofline": roof,
-            "rooflines": rooflines,
-            "phases_us": {k: v * 1e3 for k, v in avg.items()},
-            "phases_note": "per-phase CUDA events inside a second captured graph, same K, "
-                           "L2 flushed; each event node adds ~3 us",
-            "cpu_baseline": cpu,
-        }
-        if nccl is not None:
-            line["nccl_baseline"] = nccl
-        if slot_wire is not None:
-            line["wire_slot"] = slot_wire
-        if ep_only is not None:
-            line["layout_ep_only"] = ep_only
-        print(json.dumps(line), file=OUT, flush=True)
-    layer.close()
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+CONFIGS = {
+    "B": dict(H=2048, INTER=768, E=128, K=8, SHARED=0, T=8192,
+              workload="Qwen3-30B-A3B-shaped MoE layer (BASELINE configs[1]), 8192-token "
+                       "prefill, bf16 SwiGLU experts, fp32 gate logits"),
+    "C": dict(H=7168, INTER=2048, E=256, K=8, SHARED=2048, T=8192,
+              workload="DeepSeek-R1-shaped MoE layer (BASELINE configs[2]): 256 routed experts "
+                       "top-8 + a 2048-wide shared expert, fp8 e4m3 experts (per-row activation "
+                       "and per-channel weight scales), DeepSeek-V3 group-limited gate, "
+                       "8192-token prefill"),
+}
+CONFIG = "B"
+SHARED = 0
+WROW = H * 2
+WORKLOAD = CONFIGS["B"]["workload"]
+
+
+def set_config(name, tokens=None):
+    global CONFIG, H, INTER, E, K_TOP, SHARED, T_GLOBAL, WROW, WORKLOAD
+    c = CONFIGS[name]
+    CONFIG, H, INTER, E, K_TOP, SHARED = name, c["H"], c["INTER"], c["E"], c["K"], c["SHARED"]
+    T_GLOBAL = tokens or c["T"]
+    WROW = H + 16 if name == "C" else H * 2
+    WORKLOAD = c["workload"]
+
+
+def reference_layout(args):
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if args.tp == "auto" or world == 1:
+        from paper_2601_08800_b200.layer import layout_for
+        return layout_for(world, None if world == 1 else min(world, 4 if CONFIG == "C" else 2))
+    if args.tp is not None:
+        return world // int(args.tp), int(args.tp)
+    tp = min(world, 4 if CONFIG == "C" else 2)
+    return world // tp, tp
 
 
 def main():
@@ -699,19 +882,22 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tp", type=int, default=None)
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS),
+                    help="B: Qwen3-30B-A3B shape, bf16 (BASELINE configs[1], default); "
+                         "C: DeepSeek-R1 shape, fp8 + shared expert (configs[2])")
+    ap.add_argument("--tp", default=None,
+                    help="TP degree, or 'auto' (fused-layer model pick); default: the "
+                         "config's named layout")
     ap.add_argument("--tokens", type=int, default=None,
-                    help="override the global token count (default 8192, BASELINE configs[1])")
+                    help="override the global token count (default 8192)")
     ap.add_argument("--wire", default="auto", choices=["auto", "slot", "token"],
                     help="auto: token (dedup dispatch, pre-reduced combine) when n > 1")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=512)
-    ap.add_argument("--ref-sample", type=int, default=512)
+    ap.add_argument("--ref-sample", type=int, default=1024)
     args = ap.parse_args()
-    if args.tokens:
-        global T_GLOBAL
-        T_GLOBAL = args.tokens
+    set_config(args.config, args.tokens)
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3

@@ -218,6 +218,12 @@ MX_API int mx_forward(mx_plan* p, int rank, const void* x, const float* logits,
  * peer barrier's watchdog expired.  MoELayer.forward calls it after every
  * eager forward; a captured forward checks with CapturedForward.check(). */
 MX_API int mx_plan_check(mx_plan* p, int rank, void* stream);
+/* NVLink ceiling probe (bench.py's same-run denominator): this rank copies
+ * bytes_per_peer (rounded down to 4 KB) of its PARTIAL region into every
+ * peer's RECV region, 16 B loads from local HBM and 16 B stores over
+ * NVLink, all peers at once.  SPMD, W > 1; every rank should run it
+ * between the same barriers.  Clobbers RECV/PARTIAL: between forwards. */
+MX_API int mx_nvlink_probe(mx_plan* p, size_t bytes_per_peer, void* stream);
 
 /* ----- NCCL AR+A2A baseline helpers (value path of sim:598-680) -------
  * The baseline moves FULL-width rows with torch.distributed/NCCL

@@ -83,6 +83,7 @@ SIGNATURES = {
     "mx_stamp": [VP, I, I, VP],
     "mx_forward": [VP, I, VP, VP, VP, VP, C.POINTER(ExpertParams), VP, VP],
     "mx_plan_check": [VP, I, VP],
+    "mx_nvlink_probe": [VP, SZ, VP],
     "mx_baseline_dispatch_pack": [VP, I, VP, VP, VP, VP],
     "mx_baseline_dispatch_unpack": [VP, I, VP, VP],
     "mx_baseline_combine_pack": [VP, I, VP, VP, VP],

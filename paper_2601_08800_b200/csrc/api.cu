@@ -797,6 +797,18 @@ int mx_plan_check(mx_plan* p, int rank, void* stream) {
   return check_errors(p, it.first, it.last);
 }
 
+int mx_nvlink_probe(mx_plan* p, size_t bytes_per_peer, void* stream) {
+  mx_comm* c = p->comm;
+  if (c->emulate || c->W < 2) { set_error("the NVLink probe runs in SPMD mode with peers"); return MX_ERR_INVALID; }
+  bytes_per_peer &= ~(size_t)4095;
+  const size_t recv_bytes = p->off.partial - p->off.recv, part_bytes = p->off.y - p->off.partial;
+  if (bytes_per_peer == 0 || bytes_per_peer * c->W > recv_bytes || bytes_per_peer > part_bytes) {
+    set_error("probe needs 4 KB <= bytes_per_peer <= %zu", recv_bytes / c->W < part_bytes ? recv_bytes / c->W : part_bytes);
+    return MX_ERR_INVALID;
+  }
+  return launch_nvlink_probe(view_for(p, c->rank), bytes_per_peer, static_cast<cudaStream_t>(stream));
+}
+
 int mx_grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int32_t* offs,
                     const int32_t* cnts, int G, long long M_total, int N, int K, int swiglu,
                     void* stream) {

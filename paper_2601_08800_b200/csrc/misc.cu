@@ -166,3 +166,43 @@ int launch_stamp(const DevView& v, int slot, cudaStream_t s) {
 }
 
 }  // namespace mx
+
+namespace mx {
+
+// ---------------------------------------------------------------- NVLink probe
+// Same-run NVLink denominator for bench.py: every rank copies `bytes` of its
+// own PARTIAL region into every peer's RECV region (slot `rank`), 16 B
+// vector loads from local HBM and 16 B stores over NVLink -- the access mix
+// of the layer's dispatch and pre-reduction pushes.  A warp moves one 4 KB
+// chunk at a time, chunks dealt round-robin over the peers so every link
+// is busy at once.  Scratch use of RECV/PARTIAL: call between forwards only.
+__global__ void __launch_bounds__(256) k_nvlink_probe(DevView v, size_t bytes) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int peers = v.W - 1;
+  const long long per_peer = (long long)(bytes >> 12);  // 4 KB chunks per peer
+  const long long chunks = per_peer * peers;
+  const char* src = at<char>(v, v.rank, v.off.partial);
+  for (long long c = gw; c < chunks; c += nwarps) {
+    const int p = (int)(c % peers);
+    const int dst_rank = (v.rank + 1 + p) % v.W;
+    const size_t off = (size_t)(c / peers) << 12;
+    char* dst = at<char>(v, dst_rank, v.off.recv) + (size_t)v.rank * bytes + off;
+    uint4 val[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) val[q] = ld_v4(src + off + (size_t)(q * 32 + lane) * 16);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) st_v4(dst + (size_t)(q * 32 + lane) * 16, val[q]);
+  }
+}
+
+int launch_nvlink_probe(const DevView& v, size_t bytes, cudaStream_t s) {
+  if (v.W < 2) { set_error("NVLink probe needs peers"); return MX_ERR_INVALID; }
+  pdl_launch(k_nvlink_probe, 148 * 4, 256, 0, s, v, bytes);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // namespace mx

@@ -332,5 +332,6 @@ int quant_rows_e4m3(const void* src, long long lds, void* dst, long long ldd, lo
                     const int32_t* rows_dev, int cols, cudaStream_t s);
 int launch_rowsrc_slot(const DevView& v, cudaStream_t s);
 int launch_rowsrc_token(const DevView& v, cudaStream_t s);
+int launch_nvlink_probe(const DevView& v, size_t bytes, cudaStream_t s);
 
 }  // namespace mx

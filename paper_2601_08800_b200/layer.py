@@ -206,64 +206,88 @@ class MoELayer:
             self._tp_group = tp[self.group]
         return self._ep_group, self._tp_group
 
-    def forward_baseline(self, x, logits, stream=None, events=None):
+    def forward_baseline(self, x, logits, stream=None, events=None, splits=None, mark=None):
         """NCCL AR + A2A layout (sim:598-680): full-width all_to_all dispatch
         from every TP rank, the same expert kernels, full-width all_to_all
-        combine of TP partials, TP all_reduce.  Needs the send counts on the
-        host (one D2H sync), as any NCCL all_to_all_single with splits does."""
+        combine of TP partials, TP all_reduce.
+
+        NCCL's all_to_all_single needs the split sizes on the host: without
+        ``splits`` (the [n, n] send matrix S of this routing) they are read
+        back with one D2H sync, as any dynamic NCCL MoE layer does; with
+        ``splits`` nothing syncs and the call can be captured in a CUDA
+        graph (:meth:`capture_baseline`).  ``mark(name)`` / ``events`` record
+        a point after each phase: route, a2a_dispatch, expert, a2a_combine,
+        allreduce."""
         p, r, lib = self.plan, self.rank, N.load()
         s = stream or torch.cuda.current_stream()
         sp = stream_ptr(s)
         ep_g, tp_g = self._groups()
 
-        def mark(name):
-            if events is not None:
+        def _mark(name):
+            if mark is not None:
+                mark(name)
+            elif events is not None:
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(s)
                 events.append((name, ev))
 
-        mark("start")
+        _mark("start")
         p.route(logits=logits, rank=r, stream=s)
         p.barrier(stream=s)          # count rows published (our K1 exchange)
         p.layout(rank=r, stream=s)
-        send = p.rank_views(r)["send"]
-        S = send.cpu().numpy()       # host sync for the split sizes
-        mark("route")
+        S = np.asarray(splits) if splits is not None else \
+            p.rank_views(r)["send"].cpu().numpy()   # host sync for the split sizes
+        _mark("route")
         j, n, h = self.group, self.n, self.h
         send_rows = int(S[j].sum())
-        sendbuf = torch.empty(max(1, send_rows), h, dtype=self.dtype, device=x.device)
-        cnt = torch.empty(n, dtype=torch.int32, device=x.device)
-        N.check(lib.mx_baseline_dispatch_pack(p._plan, r, C.c_void_p(x.data_ptr()),
-                                              C.c_void_p(sendbuf.data_ptr()),
-                                              C.c_void_p(cnt.data_ptr()), sp), "pack")
         recv_rows = int(S[:, j].sum())
-        recvbuf = torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=x.device)
-        dist.all_to_all_single(recvbuf[:recv_rows], sendbuf[:send_rows],
-                               output_split_sizes=[int(v) for v in S[:, j]],
-                               input_split_sizes=[int(v) for v in S[j]],
+        key = (send_rows, recv_rows)
+        if getattr(self, "_bl_key", None) != key:
+            dev = x.device
+            self._bl_bufs = dict(
+                send=torch.empty(max(1, send_rows), h, dtype=self.dtype, device=dev),
+                recv=torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=dev),
+                back=torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=dev),
+                ret=torch.empty(max(1, send_rows), h, dtype=self.dtype, device=dev),
+                y=torch.empty(self.T, h, dtype=self.dtype, device=dev),
+                cnt=torch.empty(n, dtype=torch.int32, device=dev))
+            self._bl_key = key
+        b = self._bl_bufs
+        out_split = [int(v) for v in S[:, j]]
+        in_split = [int(v) for v in S[j]]
+        N.check(lib.mx_baseline_dispatch_pack(p._plan, r, C.c_void_p(x.data_ptr()),
+                                              C.c_void_p(b["send"].data_ptr()),
+                                              C.c_void_p(b["cnt"].data_ptr()), sp), "pack")
+        dist.all_to_all_single(b["recv"][:recv_rows], b["send"][:send_rows],
+                               output_split_sizes=out_split, input_split_sizes=in_split,
                                group=ep_g)
-        mark("a2a_dispatch")
-        N.check(lib.mx_baseline_dispatch_unpack(p._plan, r, C.c_void_p(recvbuf.data_ptr()),
+        _mark("a2a_dispatch")
+        N.check(lib.mx_baseline_dispatch_unpack(p._plan, r, C.c_void_p(b["recv"].data_ptr()),
                                                 sp), "unpack")
         for stage in (1, 2):  # the GEMMs only (no wire-TOKEN expand/pre-reduce)
             N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), stage, sp), "expert")
-        mark("expert")
-        back = torch.empty(max(1, recv_rows), h, dtype=self.dtype, device=x.device)
-        N.check(lib.mx_baseline_combine_pack(p._plan, r, C.c_void_p(back.data_ptr()),
-                                             C.c_void_p(cnt.data_ptr()), sp), "pack back")
-        ret = torch.empty(max(1, send_rows), h, dtype=self.dtype, device=x.device)
-        dist.all_to_all_single(ret[:send_rows], back[:recv_rows],
-                               output_split_sizes=[int(v) for v in S[j]],
-                               input_split_sizes=[int(v) for v in S[:, j]],
+        _mark("expert")
+        N.check(lib.mx_baseline_combine_pack(p._plan, r, C.c_void_p(b["back"].data_ptr()),
+                                             C.c_void_p(b["cnt"].data_ptr()), sp), "pack back")
+        dist.all_to_all_single(b["ret"][:send_rows], b["back"][:recv_rows],
+                               output_split_sizes=in_split, input_split_sizes=out_split,
                                group=ep_g)
-        mark("a2a_combine")
-        y = torch.empty(self.T, h, dtype=self.dtype, device=x.device)
-        N.check(lib.mx_baseline_combine_unpack(p._plan, r, C.c_void_p(ret.data_ptr()),
-                                               C.c_void_p(y.data_ptr()), sp), "unpack back")
+        _mark("a2a_combine")
+        N.check(lib.mx_baseline_combine_unpack(p._plan, r, C.c_void_p(b["ret"].data_ptr()),
+                                               C.c_void_p(b["y"].data_ptr()), sp), "unpack back")
         if self.m > 1:
-            dist.all_reduce(y, group=tp_g)
-        mark("allreduce")
-        return y
+            dist.all_reduce(b["y"], group=tp_g)
+        _mark("allreduce")
+        return b["y"]
+
+    def capture_baseline(self, x, logits, with_events=False):
+        """The NCCL baseline with this routing's split sizes fixed on the
+        host (read once, outside), captured as one CUDA graph like the fused
+        forward: no host sync and no per-launch CPU overhead inside, so the
+        comparison with :meth:`capture` is communicator against
+        communicator.  Falls back to eager replays of the static-split call
+        when NCCL collectives cannot be captured (``.graph`` is False)."""
+        return CapturedBaseline(self, x, logits, with_events)
 
     def close(self):
         self.plan.close()
@@ -311,6 +335,65 @@ class CapturedForward:
 
     def phase_ms(self):
         """(name, ms) per phase of the last replay (call after a sync)."""
+        return [(b, ea.elapsed_time(eb))
+                for (a, ea), (b, eb) in zip(self.events[:-1], self.events[1:])]
+
+
+class CapturedBaseline:
+    """See :meth:`MoELayer.capture_baseline`."""
+
+    def __init__(self, layer, x, logits, with_events=False):
+        self.layer, self.x, self.logits = layer, x, logits
+        self.events = []
+        self.with_events = with_events
+        layer.forward_baseline(x, logits)            # eager: split sizes, NCCL warm-up
+        p = layer.plan
+        self.splits = p.rank_views(layer.rank)["send"].cpu().numpy().copy()
+        layer.forward_baseline(x, logits, splits=self.splits)
+        torch.cuda.synchronize()
+        dist.barrier()
+        self.graph = None
+        self.error = None
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                layer.forward_baseline(x, logits, splits=self.splits)
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            dist.barrier()
+            with torch.cuda.graph(g):
+                if with_events:
+                    evs = []
+
+                    def mark(name):
+                        ev = _external_event()
+                        ev.record()
+                        evs.append((name, ev))
+                    layer.forward_baseline(x, logits, splits=self.splits, mark=mark)
+                    self.events = evs
+                else:
+                    layer.forward_baseline(x, logits, splits=self.splits)
+            torch.cuda.synchronize()
+            dist.barrier()
+            self.graph = g
+        except Exception as e:  # NCCL capture unsupported: eager static-split replays
+            self.error = f"{type(e).__name__}: {e}"[:300]
+            torch.cuda.synchronize()
+            dist.barrier()
+
+    def __call__(self):
+        if self.graph is not None:
+            self.graph.replay()
+            return self.layer._bl_bufs["y"]
+        evs = [] if self.with_events else None
+        y = self.layer.forward_baseline(self.x, self.logits, splits=self.splits, events=evs)
+        if evs is not None:
+            self.events = evs
+        return y
+
+    def phase_ms(self):
         return [(b, ea.elapsed_time(eb))
                 for (a, ea), (b, eb) in zip(self.events[:-1], self.events[1:])]
 

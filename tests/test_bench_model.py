@@ -21,7 +21,7 @@ def test_single_gpu_phases():
     T = 64
     ids = _uniform_ids(T)
     S, U = routing_stats(ids, 1, E)
-    model = bench.phase_model(S, None, 1, 1, 0, 0, T)
+    model = bench.phase_model(S, 1, 1, 0, T)
     S_d = int(S.sum())
     assert S_d == T * K
     assert model["dispatch"] == {"bound": "hbm", "bytes": T * HB + S_d * HB}
@@ -39,7 +39,7 @@ def test_token_wire_bytes_match_the_layout_model(n, m):
     ids = _uniform_ids(n * T, seed=n * 10 + m)
     S, U = routing_stats(ids, n, E)
     for group in range(n):
-        model = bench.phase_model(S, None, n, m, group, 0, T, U, "token")
+        model = bench.phase_model(S, n, m, group, T, U, "token")
         pairs = int(U[:, group].sum())
         own = int(U[group, group])
         remote_pairs = pairs - own
@@ -64,11 +64,35 @@ def test_bound_is_the_slower_of_link_and_hbm():
     n, m, T = 2, 2, 4096
     ids = _uniform_ids(n * T, seed=3)
     S, U = routing_stats(ids, n, E)
-    model = bench.phase_model(S, None, n, m, 0, 0, T, U, "token")
+    model = bench.phase_model(S, n, m, 0, T, U, "token")
     pr = model["pair_reduce"]
     # 134 MB of partial reads at 6.5 TB/s (~20 us) < 25 MB pushed at 770 GB/s (~33 us)
     assert pr["bound"] == "nvlink"
     assert pr["local_hbm_bytes"] == int(S[:, 0].sum()) * HB
     S1, U1 = routing_stats(_uniform_ids(T, seed=4), 1, E)
-    one_host = bench.phase_model(S1, None, 1, 2, 0, 0, T, U1, "token")
+    one_host = bench.phase_model(S1, 1, 2, 0, T, U1, "token")
     assert one_host["dispatch"]["bound"] == "hbm"      # one group: local expert-major copy
+
+
+def test_config_c_model_counts_the_shared_expert_and_fp8_rows():
+    """Config C (--config C): wire rows are h e4m3 bytes + a 16 B scale tail,
+    partial rows bf16, and both GEMM phases carry the TP-sharded shared
+    expert's flops next to the routed experts'."""
+    try:
+        bench.set_config("C")
+        h, It, Is, k, e = bench.H, bench.INTER, bench.SHARED, bench.K_TOP, bench.E
+        assert (h, It, Is, e, k, bench.WROW) == (7168, 2048, 2048, 256, 8, 7168 + 16)
+        rng = np.random.default_rng(1)
+        T, n, m = 128, 2, 4
+        ids = np.stack([rng.choice(e, k, replace=False) for _ in range(n * T)])
+        S, U = routing_stats(ids, n, e)
+        model = bench.phase_model(S, n, m, 0, T, U, "token")
+        S_d = int(S[:, 0].sum())
+        assert model["gemm1_swiglu"]["flops"] == 2 * S_d * h * 2 * (It // m) + 2 * T * h * 2 * (Is // m)
+        assert model["gemm2"]["flops"] == 2 * S_d * (It // m) * h + 2 * T * (Is // m) * h
+        remote_pairs = int(U[:, 0].sum() - U[0, 0])
+        disp = model["dispatch"]
+        assert disp.get("nvlink_bytes", disp["bytes"]) == remote_pairs * (h + 16)
+    finally:
+        bench.set_config("B")
+    assert bench.WROW == bench.H * 2 == 4096

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--K", type=int, default=2048)
     ap.add_argument("--swiglu", action="store_true")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--reps", type=int, default=1)
     a = ap.parse_args()
     gen = torch.Generator().manual_seed(0)
     cnts = torch.full((a.G,), a.rows, dtype=torch.int32)
@@ -42,6 +43,8 @@ def main():
     for _ in range(3):
         run()
     torch.cuda.synchronize()
+    for _ in range(a.reps - 1):
+        run()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(a.iters):
@@ -49,8 +52,14 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / a.iters * 1e3
+    try:
+        import subprocess
+        clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,temperature.gpu",
+                              "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
+    except OSError:
+        clk = "?"
     tf = 2.0 * M * a.N * a.K / (us * 1e-6) / 1e12
-    print(f"G={a.G} rows={a.rows}+-{a.jitter} N={a.N} K={a.K} swiglu={a.swiglu}: {us:8.1f} us  {tf:7.1f} TFLOP/s")
+    print(f"G={a.G} rows={a.rows}+-{a.jitter} N={a.N} K={a.K} swiglu={a.swiglu}: {us:8.1f} us  {tf:7.1f} TFLOP/s  [{clk}]")
 
 
 if __name__ == "__main__":
