@@ -185,13 +185,89 @@ __global__ void __launch_bounds__(256, 2) k_combine(DevView v) {
   if (v.sync_signal) grid_signal_and_wait(v);  // y complete on every TP rank: barrier #4
 }
 
+// One group, no TP (the single-GPU layer): every slot row is a local
+// PARTIAL row.  Warp per token; the token's slots are ordered experts
+// ascending (k_combine's order for n = 1, so the sums are the same bits)
+// and held as row pointers + weights in registers; each lane issues the
+// loads of a column vector of every slot (k x 16 B in flight) before
+// accumulating.  Registers bound the loads in flight: one column vector per
+// slot per iteration (k x 16 B per lane) at three CTAs per SM (24 warps,
+// ~96 KB in flight per SM) beats two vectors per slot at one CTA per SM
+// (153 registers; capping it at 128 spills).
+template <int KU>
+__global__ void __launch_bounds__(256, 3) k_combine_local(DevView v) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  using T = __nv_bfloat16;
+  constexpr int V = 8;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int k = v.k, h = v.h;
+  const int* ids = at<int>(v, v.rank, v.off.ids);
+  const float* wts = at<float>(v, v.rank, v.off.w);
+  const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
+  const T* part = at<T>(v, v.rank, v.off.partial);
+  T* y = at<T>(v, v.rank, v.off.y);
+  for (long long t = gw; t < v.T; t += nwarps) {
+    int e = 0x7fffffff, pos = 0;
+    float w = 0.f;
+    if (lane < k) {
+      e = ids[t * k + lane];
+      w = wts[t * k + lane];
+      pos = slot_pos[t * k + lane];
+      if (pos >= v.cap) { pos = 0; w = 0.f; }  // past capacity: never computed (mx_plan_check)
+    }
+    int rk = 0;  // rank of this slot among the token's experts (ascending)
+    for (int o = 0; o < k; ++o) {
+      const int oe = __shfl_sync(0xffffffffu, e, o);
+      rk += oe < e ? 1 : 0;
+    }
+    unsigned rp[KU];  // slot rows (32-bit: registers are the budget here)
+    float ws[KU];
+#pragma unroll
+    for (int s = 0; s < KU; ++s) {
+      const unsigned who = __ballot_sync(0xffffffffu, lane < k && rk == s);
+      const int src = who ? __ffs(who) - 1 : 0;
+      const int p = __shfl_sync(0xffffffffu, pos, src);
+      const float ww = __shfl_sync(0xffffffffu, w, src);
+      rp[s] = (unsigned)p;
+      ws[s] = who ? ww : 0.f;
+    }
+    int c = lane * V;
+    for (; c < h; c += 32 * V) {
+      uint4 raw[KU];
+#pragma unroll
+      for (int s = 0; s < KU; ++s)
+        if (s < k) raw[s] = ld_v4(part + (size_t)rp[s] * h + c);
+      float acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = 0.f;
+#pragma unroll
+      for (int s = 0; s < KU; ++s)
+        if (s < k) {
+          const T* pv = reinterpret_cast<const T*>(&raw[s]);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = fmaf(ws[s], to_acc(pv[q]), acc[q]);
+        }
+      T out[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
+      st_v4(y + (size_t)t * h + c, *reinterpret_cast<uint4*>(out));
+    }
+  }
+}
+
 template <int DT>
 static void launch_combine_dt(const DevView& v, int blocks, cudaStream_t s) {
   int c0, c1;
   col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
   const bool vec = ((size_t)c0 * v.elt) % 16 == 0 && ((size_t)(c1 - c0) * v.elt) % 16 == 0 &&
                    ((size_t)v.h * v.elt) % 16 == 0;
-  if (vec && v.k <= 8 && v.m <= 8) pdl_launch(k_combine<DT, true, 8>, blocks, 256, 0, s, v);
+  if (DT == MX_BF16 && vec && v.n == 1 && v.m == 1 && v.k <= 8 && !v.Is_t && !v.sync_wait &&
+      !v.sync_signal) {
+    long long b = (v.T + 7) / 8;
+    pdl_launch(k_combine_local<8>, (int)(b < 148 * 8 ? b : 148 * 8), 256, 0, s, v);
+  } else if (vec && v.k <= 8 && v.m <= 8) pdl_launch(k_combine<DT, true, 8>, blocks, 256, 0, s, v);
   else if (vec) pdl_launch(k_combine<DT, true, 0>, blocks, 256, 0, s, v);
   else pdl_launch(k_combine<DT, false, 0>, blocks, 256, 0, s, v);
 }
