@@ -448,6 +448,20 @@ def nvlink_probe(layer, world, reps=5, mb_per_peer=32):
                    f"{reps}, slowest rank"}
 
 
+def gemm_clocks(layer):
+    """Effective SM clock of the last GEMM launches: CTA 0 of each grouped
+    GEMM records its SM cycles and %globaltimer ns (stamp slots 56-63).
+    Sustained tensor-core load is power-capped; nvidia-smi's 50 ms samples
+    cannot see a 0.2-0.4 ms kernel's clock, this can."""
+    st = layer.plan.stamps_view(layer.rank)[56:64].cpu().numpy().astype(np.float64)
+    out = {}
+    for name, i in (("gemm1", 0), ("gemm2", 2), ("gemm1_fp8", 4), ("gemm2_fp8", 6)):
+        cyc, ns = st[i], st[i + 1]
+        if ns > 0 and cyc > 0:
+            out[name] = round(cyc / ns * 1e3, 1)
+    return out
+
+
 def timed_replays(run, steps, flush, plan_barrier, stream, world):
     """Sum of per-step CUDA-event times of ``run()`` over ``steps`` replays
     (L2 flushed and ranks aligned before each), max over ranks (ms)."""
@@ -570,12 +584,30 @@ def run_ours(args):
     phased = layer.capture(x, logits, with_events=True)
     avg = phase_avgs(phased, args.steps, flush, barrier)
     del phased
+    gemm_clk = gemm_clocks(layer)
+
+    # ---- the same forward with the NVLink phases serialized (MX_OVERLAP=0:
+    #      no side stream), for the overlap's measured effect
+    if world > 1 and wire == "token" and n > 1:
+        os.environ["MX_OVERLAP"] = "0"
+        seq = layer.capture(x, logits)
+        del os.environ["MX_OVERLAP"]
+        seq_ms = timed_replays(seq, args.steps, flush, barrier, stream, world) / args.steps
+        del seq
+        extras_pre = {"sequential_ms_per_step": seq_ms,
+                      "overlap_gain": seq_ms / ms_per_step,
+                      "overlap_note": "headline: mx_forward's overlapped schedule (dispatch, "
+                                      "expand and the other groups' pair pushes on a side "
+                                      "stream under the own-group / other-group GEMMs); "
+                                      "sequential: MX_OVERLAP=0, every phase in order"}
+    else:
+        extras_pre = {}
 
     # ---- e2e through the public API (see run_e2e)
     e2e = run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync_all)
     del runner
 
-    extras = {}
+    extras = dict(extras_pre)
     nvl = None
     if world > 1:
         nvl = nvlink_probe(layer, world)
@@ -714,6 +746,10 @@ def run_ours(args):
             "roofline": roof,
             "rooflines": rooflines,
             "phases_us": {k: v * 1e3 for k, v in avg.items()},
+            "gemm_sm_mhz": gemm_clk,
+            "gemm_sm_mhz_note": "SM clock inside the grouped GEMMs (cycles / globaltimer of "
+                                "CTA 0, last replay): the tensor phases run power-capped "
+                                "below the sampled clock",
             "phases_note": "per-phase CUDA events inside a second captured graph, same K, "
                            "L2 flushed; each event node adds ~3 us",
             "cpu_baseline": cpu,

@@ -189,6 +189,7 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   o.actq_s = take(Ist ? T * (Ist + 16) : 0);
   o.part_s = take(Ist ? T * h * 2 : 0);
   o.sh_meta = take(16);
+  o.sub = take(4 * 5 * 2 * E);
   o.total = p;
   return o;
 }
@@ -219,6 +220,10 @@ struct mx_plan {
   long long a_src_rows[MX_MAXW] = {};
   // fused device barrier flags for the next phase (mx_forward, SPMD only)
   int sync_signal = 0, sync_wait = 0;
+  // overlapped forward: the side stream the NVLink phases run on, and the
+  // fork/join events (created on first use, capturable into a CUDA graph)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[4] = {};
 };
 
 static DevView view_for(const mx_plan* p, int r) {
@@ -389,6 +394,11 @@ int mx_plan_create(mx_comm* c, const mx_plan_desc* d, mx_plan** out) {
 }
 
 int mx_plan_destroy(mx_plan* p) {
+  if (p && p->side) {
+    cudaStreamSynchronize(p->side);
+    for (cudaEvent_t e : p->ev) if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(p->side);
+  }
   delete p;
   return MX_OK;
 }
@@ -687,11 +697,97 @@ struct SyncFlags {  // sets the plan's fused-barrier flags for one phase
 };
 }  // namespace
 
+// ---------------------------------------------------------------- overlap
+// The overlapped forward (SPMD, wire TOKEN, bf16 SwiGLU experts, n > 1):
+// the NVLink phases run on a side stream under the grouped GEMMs of rows
+// that do not depend on them -- the pairwise rounds of Alg. 1/2 (sim:363-393,
+// sim:448-504) feeding compute without waiting for the whole exchange.
+//
+//   main stream                         side stream
+//   route, barrier, layout
+//   dispatch part 1 (own rows -> RECV)  -- fork -->
+//   GEMM1 on own-group sub-blocks        dispatch part 2 (pairs -> peers' XBUF,
+//                                          NVLink), barrier (rows landed), expand
+//   <-- join --
+//   GEMM1 + GEMM2 on the other groups' sub-blocks
+//                                        -- fork -->
+//   GEMM2 on own-group sub-blocks        pre-reduce + push the other groups'
+//   pre-reduce own pairs                   pairs into their owners' ZIN (NVLink)
+//   <-- join --
+//   barrier, combine, TP-group barrier
+//
+// Side-stream kernels use one 128-thread CTA per SM and no shared memory,
+// so they run on the same SMs as the persistent GEMM CTAs (213 KB smem,
+// 384 threads) instead of waiting for them.  Every row's arithmetic is the
+// non-overlapped forward's (same tiles, same sums): identical output bits.
+static bool overlap_forward(const mx_plan* p) {
+  const char* e = getenv("MX_OVERLAP");
+  if (e && e[0] == '0') return false;
+  const mx_comm* c = p->comm;
+  return !c->emulate && c->W > 1 && p->d.n_group > 1 && p->d.wire == MX_WIRE_TOKEN &&
+         p->d.expert_kind == MX_EXPERT_SWIGLU && p->d.act_dtype == MX_BF16 && !gathers(p) &&
+         p->d.tokens > 0 && !fused_barriers(p);
+}
+
+static int forward_overlapped(mx_plan* p, int rank, const void* x, const float* logits,
+                              const int32_t* ids, const void* weights, const mx_expert_params* ep,
+                              cudaStream_t s) {
+  mx_comm* c = p->comm;
+  if (!p->side) {
+    MX_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : p->ev) MX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t side = p->side;
+  int rc;
+  if ((rc = mx_route(p, rank, logits, ids, weights, s))) return rc;
+  if ((rc = barrier(p, s))) return rc;  // every group's counts published
+  if ((rc = mx_layout(p, rank, 0, s))) return rc;
+  const int r = c->rank;
+  p->a_src[r] = nullptr;
+  p->a_src_rows[r] = 0;
+  const DevView v = view_for(p, r);
+  const void* w13 = ep->w13;
+  const void* w2 = ep->w2;
+  if ((rc = launch_dispatch_token(v, x, s, 1, false))) return rc;
+  MX_CUDA(cudaEventRecord(p->ev[0], s));
+  MX_CUDA(cudaStreamWaitEvent(side, p->ev[0], 0));
+  if ((rc = launch_dispatch_token(v, x, side, 2, true))) return rc;
+  if ((rc = barrier(p, side))) return rc;  // every pair row landed
+  if ((rc = launch_expand(v, side, true))) return rc;
+  MX_CUDA(cudaEventRecord(p->ev[1], side));
+  if ((rc = launch_expert_swiglu(v, w13, w2, 1, s, 1))) return rc;
+  MX_CUDA(cudaStreamWaitEvent(s, p->ev[1], 0));
+  if ((rc = launch_expert_swiglu(v, w13, w2, 1, s, 2))) return rc;
+  if ((rc = launch_expert_swiglu(v, w13, w2, 2, s, 2))) return rc;
+  MX_CUDA(cudaEventRecord(p->ev[2], s));
+  MX_CUDA(cudaStreamWaitEvent(side, p->ev[2], 0));
+  if ((rc = launch_pair_reduce(v, side, 2, true))) return rc;
+  MX_CUDA(cudaEventRecord(p->ev[3], side));
+  if ((rc = launch_expert_swiglu(v, w13, w2, 2, s, 1))) return rc;
+  if ((rc = launch_pair_reduce(v, s, 1, false))) return rc;
+  MX_CUDA(cudaStreamWaitEvent(s, p->ev[3], 0));
+  if ((rc = barrier(p, s))) return rc;  // every owner's ZIN written
+  if ((rc = launch_combine_token(v, s))) return rc;
+  if (p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;  // y complete (TP group)
+  return MX_OK;
+}
+
 int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const int32_t* ids,
                const void* weights, const mx_expert_params* ep, void* y_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool fuse = fused_barriers(p);
   int rc;
+  if (overlap_forward(p)) {
+    RankIter it;
+    if ((rc = ranks_for(p, rank, &it))) return rc;
+    if ((rc = forward_overlapped(p, rank, x, logits, ids, weights, ep, s))) return rc;
+    if (y_out) {
+      const size_t bytes = (size_t)p->d.tokens * p->d.hidden * elt_bytes(p->d.act_dtype);
+      MX_CUDA(cudaMemcpyAsync(y_out, p->comm->heap[p->comm->rank] + p->off.y, bytes,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    return MX_OK;
+  }
   {
     SyncFlags f(p, fuse, 0, 1);
     if ((rc = mx_route(p, rank, logits, ids, weights, stream))) return rc;

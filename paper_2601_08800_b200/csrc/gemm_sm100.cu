@@ -216,7 +216,17 @@ struct Args {
   const int32_t* b_index;
   int G, N, K, ldd, out_f32;
   long long M_cap;
+  // clock probe: CTA 0 records {SM cycles, %globaltimer ns} over its
+  // lifetime -- the effective SM clock the GEMM ran at (power capping
+  // lowers it under sustained tensor load; bench.py reports it)
+  unsigned long long* clk;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Tile t -> (group, m-block, n-block) through the per-group tile prefix.
 __device__ __forceinline__ void decode_tile(int t, const int* s_tstart, int G, int nN, int* g,
@@ -310,6 +320,8 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   tc_fence_after();
   const uint32_t tmem = s_tmem;
   const int total_tiles = s_tstart[G];
+  const bool probe = args.clk && blockIdx.x == 0 && threadIdx.x == 0;
+  const unsigned long long clk0 = probe ? clock64() : 0, gt0 = probe ? globaltimer_ns() : 0;
 
   if (warp == 0 || (GATHER && warp == 3)) {
     if constexpr (GATHER) {
@@ -529,6 +541,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
 
   tc_fence_before();
   __syncthreads();
+  if (probe) {
+    args.clk[0] = clock64() - clk0;
+    args.clk[1] = globaltimer_ns() - gt0;
+  }
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -954,7 +970,10 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
     if (rc) return rc;
   }
   Args a{};
-  if (sync) { a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal; }
+  if (sync) {
+    a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal;
+    a.clk = at<unsigned long long>(*sync, sync->rank, sync->off.stamps) + (swiglu ? 56 : 58);
+  }
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
@@ -1004,7 +1023,10 @@ int grouped_gemm_fp8(const void* A, long long lda, const void* B, const float* b
   rc = make_map(&md, D, M_cap, swiglu ? N / 2 : N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
   Args a{};
-  if (sync) { a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal; }
+  if (sync) {
+    a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal;
+    a.clk = at<unsigned long long>(*sync, sync->rank, sync->off.stamps) + (swiglu ? 60 : 62);
+  }
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index;
   a.a_base = static_cast<const char*>(A); a.lda = lda; a.b_scales = b_scales;
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = 0;
@@ -1070,14 +1092,25 @@ int launch_expert_fp8(const DevView& v, const mx_expert_params& ep, int stage, c
   return rc;
 }
 
-// Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts.
+// Expert FFN of one rank: GEMM1 (+SwiGLU) then GEMM2 over its host's experts
+// -- all rows, or (sub = 1 / 2) only the own group's / the other groups'
+// sub-blocks of every expert segment (the overlapped forward runs the two
+// halves around the NVLink phases; same tiles' arithmetic, so the same bits).
 int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
-                         cudaStream_t s) {
+                         cudaStream_t s, int sub) {
   const int e0 = first_expert(v.group, v.n, v.E), e1 = first_expert(v.group + 1, v.n, v.E);
   const int El = e1 - e0;
   if (El == 0) return MX_OK;
   const int32_t* offs = at<int32_t>(v, v.rank, v.off.exp_off) + e0;
   const int32_t* cnts = at<int32_t>(v, v.rank, v.off.exp_cnt) + e0;
+  const int32_t* bidx = nullptr;
+  int G = El;
+  if (sub) {
+    const int32_t* t = at<int32_t>(v, v.rank, v.off.sub);
+    const int S = 2 * v.E;
+    if (sub == 1) { offs = t; cnts = t + S; }
+    else { offs = t + 2 * S; cnts = t + 3 * S; bidx = t + 4 * S; G = 2 * El; }
+  }
   DevView first = v, last = v;  // fused barrier: GEMM1 waits, GEMM2 signals
   first.sync_signal = 0;
   last.sync_wait = 0;
@@ -1086,12 +1119,12 @@ int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int 
     // the layout provides them, else the materialised expert-major RECV
     const void* A = v.a_src ? v.a_src : at<char>(v, v.rank, v.off.recv);
     const int32_t* rows = v.a_src ? at<int32_t>(v, v.rank, v.off.recv_src) : nullptr;
-    int rc = grouped_gemm(A, w13, at<char>(v, v.rank, v.off.act), MX_BF16, offs, cnts, nullptr, El,
+    int rc = grouped_gemm(A, w13, at<char>(v, v.rank, v.off.act), MX_BF16, offs, cnts, bidx, G,
                           v.cap, v.cap, 2 * v.I_t, v.h, 1, s, rows, v.a_src_rows, &first);
     if (rc || stage == 1) return rc;
   }
   return grouped_gemm(at<char>(v, v.rank, v.off.act), w2, at<char>(v, v.rank, v.off.partial),
-                      MX_BF16, offs, cnts, nullptr, El, v.cap, v.cap, v.h, v.I_t, 0, s, nullptr, 0,
+                      MX_BF16, offs, cnts, bidx, G, v.cap, v.cap, v.h, v.I_t, 0, s, nullptr, 0,
                       &last);
 }
 

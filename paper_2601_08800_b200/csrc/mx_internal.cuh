@@ -77,6 +77,11 @@ struct Offsets {
   size_t actq_s;      // [T][Is_t+16]
   size_t part_s;      // bf16 [T][h]     shared expert TP partial (peers read)
   size_t sh_meta;     // int32 [4]       {0, T} offs/cnt of the shared "group"
+  // source-group sub-blocks of this host's expert segments (overlapped
+  // forward): [0] own-group offs, [1] own-group counts (El each), [2]/[3]
+  // offs/counts of the rows before and after the own sub-block (2*El), [4]
+  // their local expert (GEMM b_index); stride 2*E ints
+  size_t sub;
   size_t counters;    // int32 [16]  [0]=route CTA counter [2..3]=u64 barrier epoch
   size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
   size_t stamps;      // uint64 [MX_STAMPS] %globaltimer ns written by mx_stamp
@@ -302,13 +307,20 @@ int launch_layout(const DevView& v, cudaStream_t s);
 int launch_dispatch(const DevView& v, const void* x, cudaStream_t s);
 int launch_expert_affine(const DevView& v, const void* scales, const void* biases,
                          cudaStream_t s);
+// sub: 0 every row of the host's experts, 1 the own group's sub-blocks,
+// 2 the other groups' sub-blocks (Offsets::sub)
 int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int stage,
-                         cudaStream_t s);
+                         cudaStream_t s, int sub = 0);
 int launch_expert_fp8(const DevView& v, const mx_expert_params& ep, int stage, cudaStream_t s);
 int launch_combine(const DevView& v, cudaStream_t s);
-int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s);
-int launch_expand(const DevView& v, cudaStream_t s);
-int launch_pair_reduce(const DevView& v, cudaStream_t s);
+// part: 0 every (token, host) pair, 1 the own group's pairs (local rows),
+// 2 the other groups' pairs (NVLink).  coresident: one 128-thread CTA per
+// SM, sized to share the SM with a running grouped-GEMM CTA (no shared
+// memory, <= 128 registers) -- the overlapped forward's side stream.
+int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s, int part = 0,
+                          bool coresident = false);
+int launch_expand(const DevView& v, cudaStream_t s, bool coresident = false);
+int launch_pair_reduce(const DevView& v, cudaStream_t s, int part = 0, bool coresident = false);
 int launch_combine_token(const DevView& v, cudaStream_t s);
 int launch_barrier(const DevView& v, cudaStream_t s, bool group_only = false);
 int launch_stamp(const DevView& v, int slot, cudaStream_t s);

@@ -480,8 +480,27 @@ __global__ void __launch_bounds__(512) k_layout(DevView v) {
     s_exp_off[e] -= tmp[home_of(e, n, E)];
   }
   __syncthreads();
-  if (pub)
+  if (pub) {
     for (int e = threadIdx.x; e < E; e += blockDim.x) at<int>(v, v.rank, v.off.exp_off)[e] = s_exp_off[e];
+    // source-group sub-blocks of this host's expert segments (rows grouped
+    // by source group inside each expert): the own group's block, and the
+    // blocks before / after it (the other groups' rows)
+    const int e0 = first_expert(j, n, E), e1 = first_expert(j + 1, n, E), S = 2 * E;
+    int* sub = at<int>(v, v.rank, v.off.sub);
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int i = e - e0, base = s_exp_off[e], before = s_grp_off[e], own = s_cnt[j * E + e];
+      int tot = 0;
+      for (int g = 0; g < n; ++g) tot += s_cnt[g * E + e];
+      sub[i] = base + before;
+      sub[S + i] = own;
+      sub[2 * S + 2 * i] = base;
+      sub[3 * S + 2 * i] = before;
+      sub[4 * S + 2 * i] = i;
+      sub[2 * S + 2 * i + 1] = base + before + own;
+      sub[3 * S + 2 * i + 1] = tot - before - own;
+      sub[4 * S + 2 * i + 1] = i;
+    }
+  }
   // send counts, token-major offsets, pair offsets
   for (int jd = threadIdx.x; jd < n * n; jd += blockDim.x) {
     const int g = jd / n, d = jd % n;

@@ -45,8 +45,12 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 // Warp per token: ship the row (column shard tp_rank, or the full row to the
 // own group) once per host it hits, then publish per-slot metadata to the TP
 // peer on that host: the pair's packed (slot row, weight) list and its length.
+// part: 0 every pair, 1 the own group's (local RECV rows + metadata), 2 the
+// other groups' (NVLink rows + metadata) -- the overlapped forward runs part
+// 1, then part 2 on a side stream under the own group's GEMM1.
 template <class WT>
-__global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char* __restrict__ x) {
+__global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char* __restrict__ x,
+                                                           int part) {
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   // DSPLIT warps per token, each moving its slice of the row's 16 B vectors
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char
     }
     for (int d = 0; d < n; ++d) {
       const int u = __shfl_sync(0xffffffffu, u_l, d);
-      if (u < 0) continue;
+      if (u < 0 || (part == 1 && d != v.group) || (part == 2 && d == v.group)) continue;
       if (d == v.group && direct_local) {
         // rows of this token's slots on the own host (pos < cap: layout-checked)
         const int pos = (d_l == d && p_l < v.cap) ? p_l : -1;
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char
         if (oe < e) ++idx;
       }
     }
-    if (lane < k) {
+    if (lane < k && (part == 0 || (d == v.group) == (part == 1))) {
       const int u = ud;
       const int dst = d * m + v.tp_rank;  // the TP peer that reads this metadata
       PairEnt<WT> ent;
@@ -282,8 +286,25 @@ struct ZinCursor {
 // combine fused into the pre-reduction: the owner then only reads local
 // memory); all slot loads of a column vector are issued before use.
 
+// Pair index range of a part (pairs on this host are ordered by source
+// group): 0 all, 1 the own group's [own0, own1), 2 every other group's
+// (the own range skipped).
+struct PairRange {
+  long long todo, own0, own1;
+  int part;
+  __device__ PairRange(const DevView& v, int part_) : part(part_) {
+    const int g = v.group, pairs = at<int>(v, v.rank, v.off.host_pairs)[g];
+    own0 = at<int>(v, v.rank, v.off.poff)[g * v.n + g];
+    own1 = own0 + at<int>(v, v.rank, v.off.ucnt_all)[g * v.n + g];
+    todo = part == 0 ? pairs : part == 1 ? own1 - own0 : pairs - (own1 - own0);
+  }
+  __device__ long long operator()(long long r) const {
+    return part == 0 ? r : part == 1 ? own0 + r : (r < own0 ? r : r + (own1 - own0));
+  }
+};
+
 template <int DT, class WT>
-__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
+__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v, int part) {
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
@@ -292,13 +313,14 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
+  const PairRange pr(v, part);
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
-  const T* part = at<T>(v, v.rank, v.off.partial);
+  const T* prt = at<T>(v, v.rank, v.off.partial);
   const int* ptok = at<int>(v, v.rank, v.off.pair_tok);
   const int h = v.h, sw = (h + v.m - 1) / v.m;
-  for (long long u = gw; u < pairs; u += nwarps) {
+  for (long long r = gw; r < pr.todo; r += nwarps) {
+    const long long u = pr(r);
     const int cnt = pn[u];
     const int tok = ptok[u];
     const T* rp[KU];
@@ -307,7 +329,7 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
     for (int i = 0; i < KU; ++i) {
       const PairEnt<WT> e = pe[u * v.KH + (i < cnt ? i : 0)];
       const bool ok = e.p < v.cap;  // rows past capacity were never computed
-      rp[i] = part + (size_t)(ok ? e.p : 0) * h;
+      rp[i] = prt + (size_t)(ok ? e.p : 0) * h;
       w[i] = ok ? (A)e.w : (A)0;
     }
     int c = lane * V;
@@ -351,7 +373,7 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v) {
       for (int i = 0; i < cnt; ++i) {
         const PairEnt<WT> e = pe[u * v.KH + i];
         if (e.p >= v.cap) continue;
-        const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+        const uint4 raw = ld_v4(prt + (size_t)e.p * h + c);
         const T* pv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
         for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
@@ -402,7 +424,7 @@ __host__ __device__ inline size_t prb_smem(size_t row_bytes) {
 }
 
 template <int DT>
-__global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView v) {
+__global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView v, int part) {
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
@@ -431,12 +453,13 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int pairs = at<int>(v, v.rank, v.off.host_pairs)[v.group];
-  const long long u0 = (long long)pairs * blockIdx.x / gridDim.x;
-  const long long u1 = (long long)pairs * (blockIdx.x + 1) / gridDim.x;
+  const PairRange pr(v, part);  // part 0 or 1: a contiguous pair range
+  const long long base = pr(0), pairs = pr.todo;
+  const long long u0 = base + pairs * blockIdx.x / gridDim.x;
+  const long long u1 = base + pairs * (blockIdx.x + 1) / gridDim.x;
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<float>* pe = reinterpret_cast<const PairEnt<float>*>(at<char>(v, v.rank, v.off.pair_p));
-  const T* part = at<T>(v, v.rank, v.off.partial);
+  const T* prt = at<T>(v, v.rank, v.off.partial);
   if (warp == 0) {
     const int* ptok = at<int>(v, v.rank, v.off.pair_tok);
     unsigned q = 0;
@@ -481,7 +504,7 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
           const int sl = (int)(qs % NS);
           mbar_wait(&empty[sl], ((qs / NS) & 1) ^ 1u);
           mbar_expect_tx(&full[sl], row_bytes);
-          bulk_load(slots + (size_t)sl * row_bytes, part + (size_t)ep * h, row_bytes, &full[sl]);
+          bulk_load(slots + (size_t)sl * row_bytes, prt + (size_t)ep * h, row_bytes, &full[sl]);
         }
         if (lane < PRB_KU) hdr[pi].w[lane] = ew;
         if (lane == 0) {
@@ -543,7 +566,7 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
           for (int jj = 0; jj < cnt; ++jj) {
             const PairEnt<float> e = pe[(long long)u * v.KH + jj];
             if (e.p >= v.cap) continue;
-            const uint4 raw = ld_v4(part + (size_t)e.p * h + c);
+            const uint4 raw = ld_v4(prt + (size_t)e.p * h + c);
             const T* pv = reinterpret_cast<const T*>(&raw);
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], mul_rn((A)e.w, to_acc(pv[q])));
@@ -720,20 +743,24 @@ static int check_vec(const DevView& v) {
   return MX_OK;
 }
 
-int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s) {
+int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s, int part,
+                          bool coresident) {
   int rc = check_vec(v);
   if (rc) return rc;
   if (v.T == 0) return MX_OK;
-  const int g = blocks_for((long long)v.T * DSPLIT);
-  if (v.elt == 8) pdl_launch(k_dispatch_token<double>, g, 256, 0, s, v, static_cast<const char*>(x));
-  else pdl_launch(k_dispatch_token<float>, g, 256, 0, s, v, static_cast<const char*>(x));
+  const int threads = coresident ? 128 : 256;
+  const int g = coresident ? 148 : blocks_for((long long)v.T * DSPLIT);
+  if (v.elt == 8) pdl_launch(k_dispatch_token<double>, g, threads, 0, s, v, static_cast<const char*>(x), part);
+  else pdl_launch(k_dispatch_token<float>, g, threads, 0, s, v, static_cast<const char*>(x), part);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
 
-int launch_expand(const DevView& v, cudaStream_t s) {
-  if (v.elt == 8) pdl_launch(k_expand<double>, blocks_for((long long)v.T * v.n), 256, 0, s, v);
-  else pdl_launch(k_expand<float>, blocks_for((long long)v.T * v.n), 256, 0, s, v);
+int launch_expand(const DevView& v, cudaStream_t s, bool coresident) {
+  const int threads = coresident ? 128 : 256;
+  const int g = coresident ? 148 : blocks_for((long long)v.T * v.n);
+  if (v.elt == 8) pdl_launch(k_expand<double>, g, threads, 0, s, v);
+  else pdl_launch(k_expand<float>, g, threads, 0, s, v);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
@@ -748,32 +775,34 @@ int launch_rowsrc_token(const DevView& v, cudaStream_t s) {
   return MX_OK;
 }
 
-int launch_pair_reduce(const DevView& v, cudaStream_t s) {
+int launch_pair_reduce(const DevView& v, cudaStream_t s, int part, bool coresident) {
   const size_t row_bytes = (size_t)v.h * v.elt;
   // The ring pays off for many short pairs (k/n slots per pair on
   // average): config B, 4 GPUs (k/n = 4) 60.1 vs 62.6-66 us in the layer.
   // With one host (n = 1: every pair holds all k slots) the register kernel
   // is faster: 67.6 vs 90.3 us at 2 GPUs, k = 8.  Batches too small to give
   // every SM 32 pairs (decode) keep the register kernel's single latency
-  // chain per pair.
-  if (v.elt != 8 && v.k <= 4 * v.n && (long long)v.T * v.n >= 148LL * 32 &&
-      prb_slots(row_bytes) >= PRB_KU) {
+  // chain per pair.  Its ~200 KB ring cannot share an SM with a GEMM CTA, so
+  // co-resident launches and the non-contiguous part 2 use the register kernel.
+  if (!coresident && part != 2 && v.elt != 8 && v.k <= 4 * v.n &&
+      (long long)v.T * v.n >= 148LL * 32 && prb_slots(row_bytes) >= PRB_KU) {
     auto kern = v.elt == 4 ? k_pair_reduce_bulk<MX_F32> : k_pair_reduce_bulk<MX_BF16>;
     static bool attr[2] = {false, false};
     if (!attr[v.elt == 4]) {
       MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr[v.elt == 4] = true;
     }
-    pdl_launch(kern, 148, PRB_WARPS * 32, prb_smem(row_bytes), s, v);  // one CTA per SM
+    pdl_launch(kern, 148, PRB_WARPS * 32, prb_smem(row_bytes), s, v, part);  // one CTA per SM
     MX_LAUNCH_CHECK();
     return MX_OK;
   }
   // f64 (reference association), long pairs, rows too wide to stage
-  const int g = blocks_for((long long)v.T * v.n);
+  const int threads = coresident ? 128 : 256;
+  const int g = coresident ? 148 : blocks_for((long long)v.T * v.n);
   switch (v.elt) {
-    case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, 256, 0, s, v); break;
-    case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, 256, 0, s, v); break;
-    default: pdl_launch(k_pair_reduce<MX_BF16, float>, g, 256, 0, s, v);
+    case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, threads, 0, s, v, part); break;
+    case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, threads, 0, s, v, part); break;
+    default: pdl_launch(k_pair_reduce<MX_BF16, float>, g, threads, 0, s, v, part);
   }
   MX_LAUNCH_CHECK();
   return MX_OK;

@@ -110,6 +110,17 @@ def main():
     torch.cuda.synchronize()
     if not torch.equal(y_tok, y_tok_g):
         failures.append("wire token: graph replay differs from eager")
+    # the overlapped forward (NVLink phases on a side stream under the GEMMs,
+    # n > 1) computes every row exactly as the sequential one
+    os.environ["MX_OVERLAP"] = "0"
+    y_seq = layer.forward(xs, ls).clone()
+    run_seq = layer.capture(xs, ls)
+    y_seq_g = run_seq().clone()
+    del os.environ["MX_OVERLAP"]
+    y_ovl = layer.forward(xs, ls).clone()
+    torch.cuda.synchronize()
+    if not (torch.equal(y_seq, y_tok) and torch.equal(y_seq_g, y_tok) and torch.equal(y_ovl, y_tok)):
+        failures.append("wire token: overlapped and sequential forwards differ")
     yts = gather_rows(y_tok, world)
     if rank == 0:
         oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
