@@ -155,6 +155,13 @@ MX_API int mx_comm_open_peers(mx_comm* c, const void* handles);
 MX_API int mx_comm_heap(mx_comm* c, int rank, void** base, size_t* bytes);
 MX_API int mx_comm_destroy(mx_comm* c);
 /* Device-side barrier over all ranks (SPMD; no-op when emulated).        */
+/* The device barrier in two halves that never spin, for ranks that share
+ * ONE GPU as separate processes (tests; kernels of different processes are
+ * not guaranteed to run concurrently): half 1 publishes this rank's next
+ * epoch to every peer (or TP-group peer), the caller then synchronizes the
+ * processes on the host, half 2 checks every peer's flag and sets the
+ * watchdog error word (reported by mx_plan_check) if one is missing.     */
+MX_API int mx_comm_barrier_split(mx_comm* c, int half, int group_only, void* stream);
 MX_API int mx_comm_barrier(mx_comm* c, void* stream);
 
 /* ----- layer plan ------------------------------------------------------ */

@@ -70,6 +70,7 @@ SIGNATURES = {
     "mx_comm_heap": [VP, I, PVP, PSZ],
     "mx_comm_destroy": [VP],
     "mx_comm_barrier": [VP, VP],
+    "mx_comm_barrier_split": [VP, I, I, VP],
     "mx_plan_heap_bytes": [C.POINTER(PlanDesc), PSZ],
     "mx_plan_create": [VP, C.POINTER(PlanDesc), PVP],
     "mx_plan_destroy": [VP],

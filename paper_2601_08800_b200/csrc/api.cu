@@ -64,6 +64,37 @@ __global__ void k_barrier(DevView v, int r0, int nr) {
   __threadfence_system();
 }
 
+// The barrier split in halves that never spin, for ranks that share ONE GPU
+// as separate processes (tests): nothing guarantees that kernels of
+// different processes run at the same time on one GPU, so a rank spinning
+// on a peer's flag may never see it (B200_PROFILING.md: Xid 109).  arrive
+// bumps the epoch and publishes it to the peers' flag slots; the host then
+// synchronizes the processes; verify checks (no waiting) that every peer's
+// flag holds the epoch and raises the error word otherwise.
+__global__ void k_barrier_arrive(DevView v, int r0, int nr) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
+        at<int>(v, v.rank, v.off.counters) + 2);
+    const unsigned long long epoch = ++(*ctr);
+    __threadfence_system();
+    for (int r = r0; r < r0 + nr; ++r)
+      st_release_sys(at<unsigned long long>(v, r, v.off.flags) + v.rank, epoch);
+  }
+}
+
+__global__ void k_barrier_verify(DevView v, int r0, int nr) {
+  pdl_wait();
+  const unsigned long long epoch =
+      *reinterpret_cast<volatile unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 2);
+  const int r = r0 + threadIdx.x;
+  if ((int)threadIdx.x < nr &&
+      ld_acquire_sys(at<unsigned long long>(v, v.rank, v.off.flags) + r) < epoch)
+    atomicOr(at<int>(v, v.rank, v.off.err) + 2, 1);
+  __syncthreads();
+  __threadfence_system();
+}
+
 int launch_barrier(const DevView& v, cudaStream_t s, bool group_only) {
   const int r0 = group_only ? v.group * v.m : 0, nr = group_only ? v.m : v.W;
   pdl_launch(k_barrier, 1, 64, 0, s, v, r0, nr);
@@ -433,6 +464,21 @@ int mx_plan_buffer(mx_plan* p, int rank, int which, void** ptr, size_t* bytes) {
   return MX_OK;
 }
 
+int mx_comm_barrier_split(mx_comm* c, int half, int group_only, void* stream) {
+  if (c->emulate || c->W == 1) return MX_OK;
+  if (!c->has_plan) { set_error("barrier needs a plan on the heap"); return MX_ERR_INVALID; }
+  if (half != 1 && half != 2) { set_error("half must be 1 (arrive) or 2 (verify)"); return MX_ERR_INVALID; }
+  DevView v{};
+  v.rank = c->rank; v.W = c->W; v.off = c->off;
+  for (int r = 0; r < c->W; ++r) v.heap[r] = c->heap[r];
+  const int r0 = group_only ? c->rank / c->m * c->m : 0, nr = group_only ? c->m : c->W;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (half == 1) pdl_launch(k_barrier_arrive, 1, 32, 0, s, v, r0, nr);
+  else pdl_launch(k_barrier_verify, 1, 64, 0, s, v, r0, nr);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
 int mx_comm_barrier(mx_comm* c, void* stream) {
   if (c->emulate || c->W == 1) return MX_OK;
   if (!c->has_plan) { set_error("barrier needs a plan on the heap"); return MX_ERR_INVALID; }
@@ -720,9 +766,18 @@ struct SyncFlags {  // sets the plan's fused-barrier flags for one phase
 // so they run on the same SMs as the persistent GEMM CTAs (213 KB smem,
 // 384 threads) instead of waiting for them.  Every row's arithmetic is the
 // non-overlapped forward's (same tiles, same sums): identical output bits.
+//
+// Opt-in (MX_OVERLAP=1): measured SLOWER at config B, 2 GPUs EP2 -- 0.504
+// vs 0.439 ms sequential (profiles/r02_n2_overlap_timeline.json).  Splitting
+// each grouped GEMM by source group streams every expert's weights twice
+// (403 MB per rank for GEMM1 at EP2): GEMM1 on the other groups' rows alone
+// took 124 us with nothing beside it, against ~175 us for all rows at once,
+// and the co-resident side kernels slowed the own-group halves further.
+// With ~512 rows per expert the weight traffic a split adds outweighs the
+// ~60 us of NVLink time it hides.
 static bool overlap_forward(const mx_plan* p) {
   const char* e = getenv("MX_OVERLAP");
-  if (e && e[0] == '0') return false;
+  if (!(e && e[0] == '1')) return false;
   const mx_comm* c = p->comm;
   return !c->emulate && c->W > 1 && p->d.n_group > 1 && p->d.wire == MX_WIRE_TOKEN &&
          p->d.expert_kind == MX_EXPERT_SWIGLU && p->d.act_dtype == MX_BF16 && !gathers(p) &&
@@ -739,6 +794,17 @@ static int forward_overlapped(mx_plan* p, int rank, const void* x, const float* 
   }
   cudaStream_t side = p->side;
   int rc;
+  // MX_OVERLAP_STAMPS=1: %globaltimer stamps after each step on its stream
+  // (stamp slots 30..45) for tools/overlap_timeline.py
+  const char* st_env = getenv("MX_OVERLAP_STAMPS");
+  const bool stamps = st_env && st_env[0] == '1';
+  const char* co_env = getenv("MX_OVERLAP_CORES");  // 0: full-grid side kernels (experiments)
+  const bool cores = !(co_env && co_env[0] == '0');
+  int slot = 30;
+  auto stamp = [&](cudaStream_t q) {
+    return stamps ? launch_stamp(view_for(p, c->rank), slot++, q) : MX_OK;
+  };
+  if ((rc = stamp(s))) return rc;
   if ((rc = mx_route(p, rank, logits, ids, weights, s))) return rc;
   if ((rc = barrier(p, s))) return rc;  // every group's counts published
   if ((rc = mx_layout(p, rank, 0, s))) return rc;
@@ -748,27 +814,41 @@ static int forward_overlapped(mx_plan* p, int rank, const void* x, const float* 
   const DevView v = view_for(p, r);
   const void* w13 = ep->w13;
   const void* w2 = ep->w2;
+  if ((rc = stamp(s))) return rc;                                        // 31 layout done
   if ((rc = launch_dispatch_token(v, x, s, 1, false))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 32 own rows
   MX_CUDA(cudaEventRecord(p->ev[0], s));
   MX_CUDA(cudaStreamWaitEvent(side, p->ev[0], 0));
-  if ((rc = launch_dispatch_token(v, x, side, 2, true))) return rc;
+  if ((rc = launch_dispatch_token(v, x, side, 2, cores))) return rc;
+  if ((rc = stamp(side))) return rc;                                     // 33 pushes issued
   if ((rc = barrier(p, side))) return rc;  // every pair row landed
-  if ((rc = launch_expand(v, side, true))) return rc;
+  if ((rc = stamp(side))) return rc;                                     // 34 rows landed
+  if ((rc = launch_expand(v, side, cores))) return rc;
+  if ((rc = stamp(side))) return rc;                                     // 35 expanded
   MX_CUDA(cudaEventRecord(p->ev[1], side));
   if ((rc = launch_expert_swiglu(v, w13, w2, 1, s, 1))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 36 GEMM1 own
   MX_CUDA(cudaStreamWaitEvent(s, p->ev[1], 0));
   if ((rc = launch_expert_swiglu(v, w13, w2, 1, s, 2))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 37 GEMM1 other
   if ((rc = launch_expert_swiglu(v, w13, w2, 2, s, 2))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 38 GEMM2 other
   MX_CUDA(cudaEventRecord(p->ev[2], s));
   MX_CUDA(cudaStreamWaitEvent(side, p->ev[2], 0));
-  if ((rc = launch_pair_reduce(v, side, 2, true))) return rc;
+  if ((rc = launch_pair_reduce(v, side, 2, cores))) return rc;
+  if ((rc = stamp(side))) return rc;                                     // 39 other pairs pushed
   MX_CUDA(cudaEventRecord(p->ev[3], side));
   if ((rc = launch_expert_swiglu(v, w13, w2, 2, s, 1))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 40 GEMM2 own
   if ((rc = launch_pair_reduce(v, s, 1, false))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 41 own pairs
   MX_CUDA(cudaStreamWaitEvent(s, p->ev[3], 0));
   if ((rc = barrier(p, s))) return rc;  // every owner's ZIN written
+  if ((rc = stamp(s))) return rc;                                        // 42 ZIN complete
   if ((rc = launch_combine_token(v, s))) return rc;
+  if ((rc = stamp(s))) return rc;                                        // 43 combined
   if (p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;  // y complete (TP group)
+  if ((rc = stamp(s))) return rc;                                        // 44 y complete
   return MX_OK;
 }
 

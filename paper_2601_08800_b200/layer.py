@@ -126,6 +126,43 @@ class MoELayer:
                 s.synchronize()
         return out
 
+    def forward_stepped(self, x, logits=None, ids=None, weights=None, host_barrier=None):
+        """The fused forward's phases with every device barrier replaced by
+        arrive -> host synchronization (``host_barrier()``, e.g. a gloo
+        ``dist.barrier``) -> verify: for ranks that share ONE GPU as separate
+        processes, where a kernel spinning on a peer's flag has no guarantee
+        of ever running beside the peer's kernel.  Exercises the IPC heaps,
+        peer stores/loads and the epoch-flag protocol of the SPMD layer;
+        raises through :meth:`LayerPlan.check` like :meth:`forward`."""
+        p, r = self.plan, self.rank
+        lib = N.load()
+        sp = stream_ptr(None)
+        host_barrier = host_barrier or (lambda: dist.barrier())
+
+        def bar(group=False):
+            p.barrier_split(1, group)
+            torch.cuda.synchronize()
+            host_barrier()
+            p.barrier_split(2, group)
+
+        p.route(logits=logits, ids=ids, weights=weights, rank=r)
+        bar()
+        p.layout(rank=r)
+        p.dispatch(x, rank=r)
+        bar()
+        tok = self.wire == "token"
+        stages = ([3] if tok else []) + [1, 2] + ([4] if tok else [])
+        for st in stages:
+            N.check(lib.mx_expert_stage(p._plan, r, C.byref(self.params), st, sp), "expert")
+        bar()
+        p.combine(rank=r)
+        if self.m > 1:
+            bar(group=True)
+        torch.cuda.synchronize()
+        host_barrier()
+        p.check(rank=r)
+        return self.y
+
     def forward_phases(self, x, logits, events, stream=None, event_factory=None):
         """Same launches as :meth:`forward`, phase by phase, recording a CUDA
         event after each phase (for per-kernel timing in bench.py)."""

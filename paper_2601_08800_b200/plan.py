@@ -233,6 +233,12 @@ class LayerPlan:
     def barrier(self, stream=None):
         N.check(N.load().mx_comm_barrier(self._comm, stream_ptr(stream)), "barrier")
 
+    def barrier_split(self, half, group_only=False, stream=None):
+        """Non-spinning barrier halves (1 arrive, 2 verify) for ranks sharing
+        one GPU; the caller synchronizes the processes in between."""
+        N.check(N.load().mx_comm_barrier_split(self._comm, int(half), int(group_only),
+                                               stream_ptr(stream)), "barrier")
+
     def stamp(self, slot, rank=None, stream=None):
         """Device clock (ns) into stamp ``slot`` after all earlier launches."""
         N.check(N.load().mx_stamp(self._plan, self._r(rank), int(slot), stream_ptr(stream)),
