@@ -30,6 +30,18 @@ from paper_2601_08800_b200.layer import MoELayer, layout_for  # noqa: E402
 SAME_DEVICE = False  # every rank on cuda:0 (gloo bootstrap, CUDA IPC on one device)
 
 
+def fwd(layer, x, logits=None, ids=None, weights=None):
+    """One layer forward: the fused forward with device barriers, or -- ranks
+    sharing one GPU -- the same phases with non-spinning barrier halves and a
+    host barrier between them (forward_stepped): kernels of different
+    processes on one GPU are not guaranteed to run side by side, so no rank
+    may spin on another's flag there."""
+    if SAME_DEVICE:
+        return layer.forward_stepped(x, logits, ids=ids, weights=weights,
+                                     host_barrier=dist.barrier)
+    return layer.forward(x, logits, ids=ids, weights=weights)
+
+
 def gather_rows(y, world):
     """All ranks' [T, h] outputs (device tensors under NCCL, host under gloo)."""
     if SAME_DEVICE:
@@ -73,8 +85,8 @@ def main():
     xs = torch.as_tensor(x[g * T:(g + 1) * T], device="cuda")
     ids_d = torch.as_tensor(ids[g * T:(g + 1) * T], device="cuda").contiguous()
     w_d = torch.as_tensor(w[g * T:(g + 1) * T], device="cuda").contiguous()
-    y1 = layer.forward(xs, ids=ids_d, weights=w_d).clone()
-    y2 = layer.forward(xs, ids=ids_d, weights=w_d).clone()
+    y1 = fwd(layer, xs, ids=ids_d, weights=w_d).clone()
+    y2 = fwd(layer, xs, ids=ids_d, weights=w_d).clone()
     if not torch.equal(y1, y2):
         failures.append("f64 affine: repeated forward differs")
     ys = gather_rows(y1, world)
@@ -97,29 +109,32 @@ def main():
     layer = MoELayer(n, m, T, h, E, k, I, experts=ex, rank=rank)
     xs, ls = x_all[g * T:(g + 1) * T].contiguous(), l_all[g * T:(g + 1) * T].contiguous()
     for _ in range(3):
-        y = layer.forward(xs, ls).clone()
+        y = fwd(layer, xs, ls).clone()
     y_bl = None if SAME_DEVICE else layer.forward_baseline(xs, ls).clone()
     ys = gather_rows(y, world)
     ybs = None if y_bl is None else gather_rows(y_bl, world)
     layer.close()
     # wire TOKEN (dedup dispatch + pre-reduced combine), eager and graph replay
     layer = MoELayer(n, m, T, h, E, k, I, experts=ex, rank=rank, wire="token")
-    y_tok = layer.forward(xs, ls).clone()
-    run = layer.capture(xs, ls)
-    y_tok_g = run().clone()
-    torch.cuda.synchronize()
-    if not torch.equal(y_tok, y_tok_g):
-        failures.append("wire token: graph replay differs from eager")
-    # the overlapped forward (NVLink phases on a side stream under the GEMMs,
-    # n > 1) computes every row exactly as the sequential one
-    os.environ["MX_OVERLAP"] = "1"
-    y_ovl = layer.forward(xs, ls).clone()
-    run_ovl = layer.capture(xs, ls)
-    y_ovl_g = run_ovl().clone()
-    del os.environ["MX_OVERLAP"]
-    torch.cuda.synchronize()
-    if not (torch.equal(y_ovl, y_tok) and torch.equal(y_ovl_g, y_tok)):
-        failures.append("wire token: overlapped and sequential forwards differ")
+    y_tok = fwd(layer, xs, ls).clone()
+    if not SAME_DEVICE:
+        run = layer.capture(xs, ls)
+        y_tok_g = run().clone()
+        torch.cuda.synchronize()
+        if not torch.equal(y_tok, y_tok_g):
+            failures.append("wire token: graph replay differs from eager")
+        # the opt-in overlapped forward (NVLink phases on a side stream under
+        # the GEMMs, n > 1) computes every row exactly as the sequential one
+        os.environ["MX_OVERLAP"] = "1"
+        y_ovl = layer.forward(xs, ls).clone()
+        run_ovl = layer.capture(xs, ls)
+        y_ovl_g = run_ovl().clone()
+        del os.environ["MX_OVERLAP"]
+        torch.cuda.synchronize()
+        if not (torch.equal(y_ovl, y_tok) and torch.equal(y_ovl_g, y_tok)):
+            failures.append("wire token: overlapped and sequential forwards differ")
+    elif not torch.equal(y_tok, fwd(layer, xs, ls)):
+        failures.append("wire token: repeated stepped forward differs")
     yts = gather_rows(y_tok, world)
     if rank == 0:
         oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
@@ -153,7 +168,7 @@ def main():
     outs = {}
     for wire in ("slot", "token"):
         layer = MoELayer(n, m, T, h, E, k, I, experts=fex, rank=rank, wire=wire)
-        outs[wire] = gather_rows(layer.forward(xs8, ls8).clone(), world)
+        outs[wire] = gather_rows(fwd(layer, xs8, ls8).clone(), world)
         layer.close()
     if rank == 0:
         gate, up, down, shared = fex.oracle_arrays(n, m)
@@ -169,6 +184,21 @@ def main():
                 if fro > 1e-2 or mx > 5e-2:
                     failures.append(f"fp8 {wire} rank {r}: fro {fro:.3e} max {mx:.3e}")
         print(f"fp8 layer checked over slot/token wires", flush=True)
+
+    # ---------------- capacity below the routed rows: every rank raises
+    from paper_2601_08800_b200 import CapacityError
+    T, h, E, k, I = 64, 256, 16, 4, 256
+    layer = MoELayer(n, m, T, h, E, k, I, experts=SwiGLUExperts.random(E, h, I, seed=5),
+                     rank=rank, wire="token", capacity=T // 2)
+    xc = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    lc = torch.randn(T, E, device="cuda", generator=gen)
+    try:
+        fwd(layer, xc, lc)
+        failures.append(f"rank {rank}: capacity {T // 2} overflow not raised")
+    except CapacityError as e:
+        if "routed slots, capacity" not in str(e):
+            failures.append(f"rank {rank}: capacity message {e}")
+    layer.close()
 
     flag = torch.tensor([len(failures)], device="cpu" if SAME_DEVICE else "cuda")
     dist.all_reduce(flag)

@@ -1,13 +1,14 @@
 """Launch the SPMD parity check on every multi-GPU world the box offers, and
 on one GPU with every rank a separate process on cuda:0.
 
-The one-device form runs the real SPMD machinery -- per-process heaps
-exchanged as CUDA IPC handles, the system-scope flag barriers with their
-device epochs, graph capture and replay across processes -- on any box with
-one GPU (gloo bootstraps it; only the NCCL baseline arm is skipped).  The
-GPU time-slices the ranks' contexts, so each barrier waits for the other
-processes to be scheduled: slow, but exactly the cross-process ordering the
-multi-GPU layer depends on."""
+The one-device form runs the SPMD layer's machinery -- per-process heaps
+exchanged as CUDA IPC handles, peer stores and loads through those
+mappings, the epoch-flag barrier protocol -- on any box with one GPU (gloo
+bootstraps it).  Kernels of different processes are not guaranteed to run
+side by side on one GPU, so there no rank spins on another's flag: every
+device barrier is split into a publishing half and a checking half with a
+host barrier between them (MoELayer.forward_stepped); graph replay, the
+opt-in overlapped schedule and the NCCL arm run only with one GPU per rank."""
 import os
 import subprocess
 import sys
@@ -38,9 +39,9 @@ def _run(nproc, tp=None, env=None, port_off=0, same_device=False):
 
 @pytest.mark.parametrize("nproc,tp", [(2, 1), (2, 2), (4, 2), (4, 4), (8, 2), (8, 4)])
 def test_spmd_layer_one_device(nproc, tp):
-    """nproc ranks as processes on cuda:0: IPC heaps, device barriers, graph
-    replay, f64 bit-exact / bf16 / fp8 parity, both wires (the 8-rank layouts
-    are config B's TP2 x EP4 and config C's TP4 x EP2)."""
+    """nproc ranks as processes on cuda:0: IPC heaps, split barriers, f64
+    bit-exact / bf16 / fp8 parity, both wires, capacity errors on every rank
+    (the 8-rank layouts are config B's TP2 x EP4 and config C's TP4 x EP2)."""
     if torch.cuda.device_count() < 1:
         pytest.skip("needs a GPU")
     out = _run(nproc, tp, port_off=100, same_device=True)
