@@ -70,7 +70,7 @@ __global__ void k_bl_dispatch_unpack(DevView v, const char* recv) {
     s_dyn[j * (El + 1) + El] = run;
   }
   __syncthreads();
-  const int rows = at<int>(v, v.rank, v.off.host_rows)[d];
+  const int rows = (int)min((long long)at<int>(v, v.rank, v.off.host_rows)[d], v.cap);
   const size_t row = (size_t)v.h * v.elt;
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -112,7 +112,7 @@ __global__ void k_bl_combine_pack(DevView v, char* send, int32_t* counts) {
     for (int j = threadIdx.x; j < v.n; j += blockDim.x)
       counts[j] = at<int>(v, v.rank, v.off.send)[j * v.n + d];
   __syncthreads();
-  const int rows = at<int>(v, v.rank, v.off.host_rows)[d];
+  const int rows = (int)min((long long)at<int>(v, v.rank, v.off.host_rows)[d], v.cap);
   const size_t row = (size_t)v.h * v.elt;
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;

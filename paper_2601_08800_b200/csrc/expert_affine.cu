@@ -22,7 +22,8 @@ k_expert_affine(DevView v, const typename Elt<DT>::Acc* __restrict__ scales,
   const int e0 = first_expert(d, v.n, v.E), e1 = first_expert(d + 1, v.n, v.E);
   const int ne = e1 - e0;
   const int* exp_off = at<int>(v, v.rank, v.off.exp_off);
-  const int rows = at<int>(v, v.rank, v.off.host_rows)[d];
+  // rows past capacity were never received (flagged by the layout)
+  const int rows = (int)min((long long)at<int>(v, v.rank, v.off.host_rows)[d], v.cap);
   for (int i = threadIdx.x; i < ne; i += blockDim.x) s_off[i] = exp_off[e0 + i];
   __syncthreads();
   int c0, c1;

@@ -446,8 +446,10 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
       const int cnt = s_cnt[g];
       const int r_local = mb * BM + row_in_tile;
-      const bool valid = r_local < cnt;
       const long long row = (long long)s_off[g] + r_local;
+      // rows past M_cap (a host over capacity, flagged by the layout) are
+      // never written: TMA drops them from full boxes, direct stores skip them
+      const bool valid = r_local < cnt && row < args.M_cap;
       // the warp's 32 rows all belong to this group -> TMA box store
       const bool full_box = !args.out_f32 && (mb * BM + q * 32 + 31) < cnt;
       const int row0 = s_off[g] + mb * BM + q * 32;
@@ -750,8 +752,10 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
       decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
       const int cnt = s_cnt[g];
       const int r_local = mb * PM + (int)crank * 128 + row_in_half;
-      const bool valid = r_local < cnt;
       const long long row = (long long)s_off[g] + r_local;
+      // rows past M_cap (a host over capacity, flagged by the layout) are
+      // never written: TMA drops them from full boxes, direct stores skip them
+      const bool valid = r_local < cnt && row < args.M_cap;
       const bool full_box = (mb * PM + (int)crank * 128 + q * 32 + 31) < cnt;
       const int row0 = s_off[g] + mb * PM + (int)crank * 128 + q * 32;
       mbar_wait(&tfull[acc], acc_phase);

@@ -17,7 +17,8 @@ k_quant_rows(const __nv_bfloat16* __restrict__ src, long long lds, unsigned char
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const long long R = rows_dev ? (long long)*rows_dev : rows;
+  // rows_dev: the live row count (a host's routed rows), clamped to the buffer's
+  const long long R = rows_dev ? min((long long)*rows_dev, rows) : rows;
   for (long long r = gw; r < R; r += nw) {
     const __nv_bfloat16* s = src + r * lds;
     float amax = 0.f;

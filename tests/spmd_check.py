@@ -187,7 +187,7 @@ def main():
 
     # ---------------- capacity below the routed rows: every rank raises
     from paper_2601_08800_b200 import CapacityError
-    T, h, E, k, I = 64, 256, 16, 4, 256
+    T, h, E, k, I = 64, 256, 16, 4, 512
     layer = MoELayer(n, m, T, h, E, k, I, experts=SwiGLUExperts.random(E, h, I, seed=5),
                      rank=rank, wire="token", capacity=T // 2)
     xc = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
