@@ -785,7 +785,7 @@ def run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync
     l_h = logits.cpu().pin_memory()
     y_hs = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
     copy_out = tp == 0
-    xs, ls = [x, torch.empty_like(x)], [logits, torch.empty_like(logits)]
+    xs, ls = [x, x.clone()], [logits, logits.clone()]   # second graph's buffers (valid tokens)
     runners = [runner, layer.capture(xs[1], ls[1])]
     y_stage = [torch.empty(T, H, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
