@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(256, 3) k_combine_local(DevView v) {
   const float* wts = at<float>(v, v.rank, v.off.w);
   const int* slot_pos = at<int>(v, v.rank, v.off.slot_pos);
   const T* part = at<T>(v, v.rank, v.off.partial);
+  const T* part_s = at<T>(v, v.rank, v.off.part_s);
   T* y = at<T>(v, v.rank, v.off.y);
   for (long long t = gw; t < v.T; t += nwarps) {
     int e = 0x7fffffff, pos = 0;
@@ -249,6 +250,12 @@ __global__ void __launch_bounds__(256, 3) k_combine_local(DevView v) {
 #pragma unroll
           for (int q = 0; q < V; ++q) acc[q] = fmaf(ws[s], to_acc(pv[q]), acc[q]);
         }
+      if (v.Is_t) {  // shared expert (weight 1), after the routed slots as in k_combine
+        const uint4 sraw = ld_v4(part_s + (size_t)t * h + c);
+        const T* pv = reinterpret_cast<const T*>(&sraw);
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
+      }
       T out[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
@@ -263,7 +270,7 @@ static void launch_combine_dt(const DevView& v, int blocks, cudaStream_t s) {
   col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
   const bool vec = ((size_t)c0 * v.elt) % 16 == 0 && ((size_t)(c1 - c0) * v.elt) % 16 == 0 &&
                    ((size_t)v.h * v.elt) % 16 == 0;
-  if (DT == MX_BF16 && vec && v.n == 1 && v.m == 1 && v.k <= 8 && !v.Is_t && !v.sync_wait &&
+  if (DT == MX_BF16 && vec && v.n == 1 && v.m == 1 && v.k <= 8 && !v.sync_wait &&
       !v.sync_signal) {
     long long b = (v.T + 7) / 8;
     pdl_launch(k_combine_local<8>, (int)(b < 148 * 8 ? b : 148 * 8), 256, 0, s, v);

@@ -35,6 +35,13 @@ constexpr int NUM_THREADS_1 = 384;    // single-CTA kernel: warps 4..11 = 8 epil
 constexpr int GATHER_THREADS = 64;    // gathered A: warps 0 and 3 issue the row LDGSTS
 constexpr int GATHER_LAG = 2;         // stages a gathering thread runs ahead of its arrive
 
+#ifndef MX_GEMM_TPF       // next-tile k-blocks prefetched into L2 (0: off)
+#define MX_GEMM_TPF 0
+#endif
+#ifndef MX_GEMM_TPF_LEAD  // ... issued this many k-blocks before the tile's last load
+#define MX_GEMM_TPF_LEAD 4
+#endif
+
 template <int BN>
 struct Cfg {
   static constexpr int STAGES = BN == 256 ? 4 : 6;
@@ -68,6 +75,13 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// L2 prefetch of a TMA box (no shared memory, no completion).
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1)
+               : "memory");
 }
 
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -383,7 +397,12 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       for (int j = (issued < GATHER_LAG ? issued : GATHER_LAG); j >= 1; --j)
         mbar_arrive(&full[(stage + C::STAGES - j) % C::STAGES]);
     } else if (lane == 0) {
-      // ===== TMA producer
+      // ===== TMA producer.  The first k-blocks of a tile are the MMA warp's
+      // stall point (new rows / a new expert's weights, cold in L2: ncu
+      // samples the MMA warp waiting on the tile's first stage, the ring
+      // only covers STAGES k-blocks); TPF k-blocks of the next tile's A and
+      // B boxes are prefetched into L2 TPF_LEAD k-blocks before this tile's
+      // last load is issued.
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
@@ -392,7 +411,19 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         const int a_row = s_off[g] + mb * BM;
         const int bg = args.b_index ? args.b_index[g] : g;
         const int b_row = bg * args.N + nb * BN;
+        const int tn = t + (int)gridDim.x;
+        const int pf_at = kblocks > MX_GEMM_TPF_LEAD ? kblocks - MX_GEMM_TPF_LEAD : 0;
         for (int kb = 0; kb < kblocks; ++kb) {
+          if (MX_GEMM_TPF > 0 && kb == pf_at && tn < total_tiles) {
+            int g2, mb2, nb2;
+            decode_tile(tn, s_tstart, G, nN, &g2, &mb2, &nb2);
+            const int a2 = s_off[g2] + mb2 * BM;
+            const int b2 = (args.b_index ? args.b_index[g2] : g2) * args.N + nb2 * BN;
+            for (int q = 0; q < MX_GEMM_TPF && q < kblocks; ++q) {
+              tma_prefetch_l2(&map_a, q * KE, a2);
+              tma_prefetch_l2(&map_b, q * KE, b2);
+            }
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * KE, a_row);
