@@ -1,7 +1,7 @@
-# next-tile L2 prefetch variants of the grouped GEMM, A/B interleaved to share box drift
+# warp-3 L2 prefetch variants of the grouped GEMM, A/B interleaved to share box drift
 L=paper_2601_08800_b200/lib
 for rep in 1 2; do
-for lib in $L/libmixserve_b200.so $L/variants/libmx_tpf*.so; do
+for lib in $L/libmixserve_b200.so $L/variants/libmx_w3pf*.so; do
   echo "== $lib"
   export MIXSERVE_B200_LIB=$lib
   python tools/gemm_bench.py --G 128 --rows 512 --jitter 56 --N 1536 --K 2048 --swiglu --reps 5
