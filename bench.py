@@ -707,6 +707,17 @@ def run_ours(args):
                      nominal=900.0, frac_nominal=spec["bytes"] / sec / 1e9 / 900.0)
         r["frac"] = r["achieved"] / r["peak"]
         rooflines[ph] = r
+    # the tensor phases' peak at the clock they actually ran at (gemm_sm_mhz,
+    # power capped): context for the burst fraction, not a replacement
+    for ph, key in (("gemm1_swiglu", "gemm1"), ("gemm2", "gemm2")):
+        if CONFIG == "C":
+            key += "_fp8"
+        r = rooflines.get(ph)
+        mhz = gemm_clk.get(key)
+        if r and mhz:
+            r["peak_at_gemm_clock"] = r["peak"] * mhz / 1965.0
+            r["frac_at_gemm_clock"] = r["achieved"] / r["peak_at_gemm_clock"]
+            r["gemm_sm_mhz"] = mhz
     dom = max(rooflines, key=lambda k: rooflines[k]["us"]) if rooflines else None
     roof = dict(rooflines[dom]) if dom else None
     if roof is not None:
