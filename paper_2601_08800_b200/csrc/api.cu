@@ -882,6 +882,23 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
     if ((rc = mx_dispatch(p, rank, x, stream))) return rc;
   }
   if (!fuse && (rc = barrier(p, s))) return rc;  // every row landed
+  // the token wire's combine side as one persistent kernel (pre-reduction,
+  // exchange barrier, combine: k_reduce_combine) where it applies
+  const char* rc_env = getenv("MX_FUSED_COMBINE");
+  const bool fused_combine = !fuse && !(rc_env && rc_env[0] == '0') && !p->comm->emulate &&
+                             p->d.wire == MX_WIRE_TOKEN && reduce_combine_ok(view_for(p, p->comm->rank));
+  if (fused_combine) {
+    for (int st : {3, 1, 2})
+      if ((rc = mx_expert_stage(p, rank, ep, st, stream))) return rc;
+    if ((rc = launch_reduce_combine(view_for(p, p->comm->rank), s))) return rc;
+    if (p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;  // y complete (TP group)
+    if (y_out) {
+      const size_t bytes = (size_t)p->d.tokens * p->d.hidden * elt_bytes(p->d.act_dtype);
+      MX_CUDA(cudaMemcpyAsync(y_out, p->comm->heap[p->comm->rank] + p->off.y, bytes,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    return MX_OK;
+  }
   {
     SyncFlags f(p, fuse, 1, 1);
     if ((rc = mx_expert(p, rank, ep, stream))) return rc;

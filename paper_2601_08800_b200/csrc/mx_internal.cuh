@@ -322,6 +322,8 @@ int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s, int p
 int launch_expand(const DevView& v, cudaStream_t s, bool coresident = false);
 int launch_pair_reduce(const DevView& v, cudaStream_t s, int part = 0, bool coresident = false);
 int launch_combine_token(const DevView& v, cudaStream_t s);
+int launch_reduce_combine(const DevView& v, cudaStream_t s);
+bool reduce_combine_ok(const DevView& v);
 int launch_barrier(const DevView& v, cudaStream_t s, bool group_only = false);
 int launch_stamp(const DevView& v, int slot, cudaStream_t s);
 int launch_baseline_dispatch_pack(const DevView& v, const void* x, void* send,

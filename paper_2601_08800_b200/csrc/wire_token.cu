@@ -424,8 +424,7 @@ __host__ __device__ inline size_t prb_smem(size_t row_bytes) {
 }
 
 template <int DT>
-__global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView v, int part) {
-  pdl_wait();  // predecessor's outputs are visible after this
+__device__ __forceinline__ void prb_body(const DevView& v, int part) {
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
@@ -579,6 +578,12 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
       }
     }
   }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView v, int part) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  prb_body<DT>(v, part);
   if (v.sync_signal) grid_signal(v);  // every owner's ZIN written: barrier #3
 }
 
@@ -586,9 +591,7 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
 // (j-1, ..., j) of the pre-reduced partials the hosts pushed into this rank's
 // ZIN; then push the shard to every TP rank of the group (final all-gather).
 template <int DT>
-__global__ void __launch_bounds__(256) k_combine_token(DevView v) {
-  pdl_wait();  // predecessor's outputs are visible after this
-  if (v.sync_wait) grid_wait(v);  // every host's pushes into ZIN have landed
+__device__ __forceinline__ void combine_token_body(const DevView& v) {
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
@@ -703,7 +706,62 @@ __global__ void __launch_bounds__(256) k_combine_token(DevView v) {
         st_v4(at<T>(v, j * m + tt, v.off.y) + (size_t)t * h + c, *reinterpret_cast<uint4*>(out));
     }
   }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_combine_token(DevView v) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  if (v.sync_wait) grid_wait(v);  // every host's pushes into ZIN have landed
+  combine_token_body<DT>(v);
   if (v.sync_signal) grid_signal_and_wait(v);  // y complete on every TP rank: barrier #4
+}
+
+// The combine side as ONE persistent kernel (one CTA per SM, all resident):
+// the pair pre-reduction pushes every pair row's column shards into the
+// owners' ZIN over NVLink, the grid meets at an exchange barrier -- the last
+// CTA to finish publishes this rank's epoch to every peer and alone polls
+// the peers' flags, the other CTAs poll one local flag it raises -- and the
+// same CTAs then sum their local ZIN planes and push y's shard to the TP
+// peers.  Replaces pre-reduction kernel -> barrier kernel -> combine kernel
+// (two kernel boundaries and the standalone barrier's launch).
+__device__ __forceinline__ void exchange_barrier(const DevView& v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* cnt = reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 4;
+    unsigned long long* go = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 8);
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(epoch_ctr(v)) + 1;
+    __threadfence_system();  // this CTA's pushes ordered before its arrival
+    const long long t0 = clock64();
+    if (atomicAdd(cnt, 1) == (int)gridDim.x - 1) {
+      *cnt = 0;
+      __threadfence_system();
+      *epoch_ctr(v) = e;
+      for (int r = 0; r < v.W; ++r)
+        st_release_sys(reinterpret_cast<unsigned long long*>(v.heap[r] + v.off.flags) + v.rank, e);
+      const unsigned long long* mine = reinterpret_cast<const unsigned long long*>(v.heap[v.rank] + v.off.flags);
+      for (int r = 0; r < v.W; ++r)
+        while (ld_acquire_sys(mine + r) < e)
+          if (clock64() - t0 > 20000000000LL) { atomicOr(reinterpret_cast<int*>(v.heap[v.rank] + v.off.err) + 2, 1); break; }
+      __threadfence_system();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(go), "l"(e) : "memory");
+    } else {
+      unsigned long long g = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(g) : "l"(go) : "memory");
+        if (clock64() - t0 > 20000000000LL) { atomicOr(reinterpret_cast<int*>(v.heap[v.rank] + v.off.err) + 2, 1); break; }
+      } while (g < e);
+    }
+  }
+  __syncthreads();
+}
+
+template <int DT>
+__global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_reduce_combine(DevView v) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  prb_body<DT>(v, 0);
+  exchange_barrier(v);  // every host's pushes into this rank's ZIN have landed
+  combine_token_body<DT>(v);
 }
 
 // Gathered GEMM1 (SwiGLU): the row table replaces the expansion copy --
@@ -805,6 +863,44 @@ int launch_pair_reduce(const DevView& v, cudaStream_t s, int part, bool coreside
     default: pdl_launch(k_pair_reduce<MX_BF16, float>, g, threads, 0, s, v, part);
   }
   MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+// The fused combine side (k_reduce_combine) where the bulk pre-reduction
+// applies; returns MX_ERR_UNSUPPORTED otherwise (the caller then launches
+// pre-reduction, barrier and combine separately).  Cooperative launch: the
+// exchange barrier needs every CTA resident.
+bool reduce_combine_ok(const DevView& v) {
+  const size_t row_bytes = (size_t)v.h * v.elt;
+  return !(v.elt == 8 || v.k > 4 * v.n || (long long)v.T * v.n < 148LL * 32 ||
+           prb_slots(row_bytes) < PRB_KU || v.T == 0 || v.W < 2);
+}
+
+int launch_reduce_combine(const DevView& v, cudaStream_t s) {
+  const size_t row_bytes = (size_t)v.h * v.elt;
+  if (!reduce_combine_ok(v)) return MX_ERR_UNSUPPORTED;
+  int rc = check_vec(v);
+  if (rc) return rc;
+  auto kern = v.elt == 4 ? k_reduce_combine<MX_F32> : k_reduce_combine<MX_BF16>;
+  static bool attr[2] = {false, false};
+  if (!attr[v.elt == 4]) {
+    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr[v.elt == 4] = true;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(PRB_WARPS * 32);
+  cfg.dynamicSmemBytes = prb_smem(row_bytes);
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  MX_CUDA(cudaLaunchKernelEx(&cfg, kern, v));
   return MX_OK;
 }
 

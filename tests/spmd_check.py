@@ -135,6 +135,36 @@ def main():
             failures.append("wire token: overlapped and sequential forwards differ")
     elif not torch.equal(y_tok, fwd(layer, xs, ls)):
         failures.append("wire token: repeated stepped forward differs")
+    # larger token-wire batch (>= 32 pairs per SM): the combine side runs as
+    # one persistent kernel (k_reduce_combine); identical bits to the three
+    # separate launches (MX_FUSED_COMBINE=0), eager and in a graph
+    if not SAME_DEVICE:
+        Tb = 2560
+        xb = torch.randn(n * Tb, h, device="cuda", generator=gen).to(torch.bfloat16)
+        lb = torch.randn(n * Tb, E, device="cuda", generator=gen)
+        xbs, lbs = xb[g * Tb:(g + 1) * Tb].contiguous(), lb[g * Tb:(g + 1) * Tb].contiguous()
+        big = MoELayer(n, m, Tb, h, E, k, I, experts=ex, rank=rank, wire="token")
+        yf = big.forward(xbs, lbs).clone()
+        yfg = big.capture(xbs, lbs)().clone()
+        os.environ["MX_FUSED_COMBINE"] = "0"
+        ys3 = big.forward(xbs, lbs).clone()
+        del os.environ["MX_FUSED_COMBINE"]
+        torch.cuda.synchronize()
+        if not (torch.equal(yf, ys3) and torch.equal(yfg, ys3)):
+            failures.append("fused combine kernel differs from the separate launches")
+        ybig = gather_rows(yf, world)
+        big.close()
+        if rank == 0:
+            oexb = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
+                                    ex.w_down.float().cpu().numpy())
+            idsb, wb = orc.router_topk(lb.cpu().numpy(), k)
+            samp = np.arange(0, n * Tb, 7)
+            y_refb = orc.moe_layer_swiglu(xb.float().cpu().numpy()[samp], idsb[samp], wb[samp], oexb)
+            got = torch.cat([ybig[r * m] for r in range(n)]).float().cpu().numpy()[samp]
+            eb = orc.verify_metric(got, y_refb)
+            print(f"fused-combine batch ({Tb} tokens/group): err {eb:.3e}", flush=True)
+            if eb > 2e-2:
+                failures.append(f"fused combine: err {eb:.3e}")
     yts = gather_rows(y_tok, world)
     if rank == 0:
         oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
