@@ -882,10 +882,14 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
     if ((rc = mx_dispatch(p, rank, x, stream))) return rc;
   }
   if (!fuse && (rc = barrier(p, s))) return rc;  // every row landed
-  // the token wire's combine side as one persistent kernel (pre-reduction,
-  // exchange barrier, combine: k_reduce_combine) where it applies
+  // opt-in (MX_FUSED_COMBINE=1): the token wire's combine side as one
+  // persistent kernel (pre-reduction, exchange barrier, combine:
+  // k_reduce_combine) where it applies.  Bit-identical to the three
+  // launches and measured equal at config B, 2 GPUs EP2 (0.4421 vs 0.4420
+  // ms): the two kernel boundaries it removes cost what its cooperative
+  // launch (no programmatic dependent launch) and in-kernel barrier add.
   const char* rc_env = getenv("MX_FUSED_COMBINE");
-  const bool fused_combine = !fuse && !(rc_env && rc_env[0] == '0') && !p->comm->emulate &&
+  const bool fused_combine = !fuse && (rc_env && rc_env[0] == '1') && !p->comm->emulate &&
                              p->d.wire == MX_WIRE_TOKEN && reduce_combine_ok(view_for(p, p->comm->rank));
   if (fused_combine) {
     for (int st : {3, 1, 2})

@@ -135,20 +135,20 @@ def main():
             failures.append("wire token: overlapped and sequential forwards differ")
     elif not torch.equal(y_tok, fwd(layer, xs, ls)):
         failures.append("wire token: repeated stepped forward differs")
-    # larger token-wire batch (>= 32 pairs per SM): the combine side runs as
-    # one persistent kernel (k_reduce_combine); identical bits to the three
-    # separate launches (MX_FUSED_COMBINE=0), eager and in a graph
+    # larger token-wire batch (>= 32 pairs per SM): the combine side as one
+    # persistent kernel (opt-in k_reduce_combine) gives the bits of the
+    # three separate launches, eager and in a graph
     if not SAME_DEVICE:
         Tb = 2560
         xb = torch.randn(n * Tb, h, device="cuda", generator=gen).to(torch.bfloat16)
         lb = torch.randn(n * Tb, E, device="cuda", generator=gen)
         xbs, lbs = xb[g * Tb:(g + 1) * Tb].contiguous(), lb[g * Tb:(g + 1) * Tb].contiguous()
         big = MoELayer(n, m, Tb, h, E, k, I, experts=ex, rank=rank, wire="token")
+        os.environ["MX_FUSED_COMBINE"] = "1"
         yf = big.forward(xbs, lbs).clone()
         yfg = big.capture(xbs, lbs)().clone()
-        os.environ["MX_FUSED_COMBINE"] = "0"
-        ys3 = big.forward(xbs, lbs).clone()
         del os.environ["MX_FUSED_COMBINE"]
+        ys3 = big.forward(xbs, lbs).clone()
         torch.cuda.synchronize()
         if not (torch.equal(yf, ys3) and torch.equal(yfg, ys3)):
             failures.append("fused combine kernel differs from the separate launches")
