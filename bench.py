@@ -814,40 +814,46 @@ def run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync
             ls[b].copy_(l_h, non_blocking=True)
         ev_in[b].record(h2d_s)
 
-    sync_all()
-    flush.fill_(1)
-    layer.plan.barrier()
-    e_a = torch.cuda.Event(enable_timing=True)
-    e_b = torch.cuda.Event(enable_timing=True)
-    e_a.record(stream)
-    h2d_s.wait_event(e_a)
-    d2h_s.wait_event(e_a)
-    h2d_step(0)
-    for i in range(args.steps):
-        b = i % 2
-        if i + 1 < args.steps:
-            h2d_step(i + 1)
-        stream.wait_event(ev_in[b])
-        y = runners[b]()                           # the captured forward
-        ev_free[b].record(stream)
-        if copy_out:
-            if i >= 2:
-                stream.wait_event(ev_d2h[b])       # y_stage[b] drained to host
-            y_stage[b].copy_(y, non_blocking=True)
-            ev_out[b].record(stream)
-            d2h_s.wait_event(ev_out[b])
-            with torch.cuda.stream(d2h_s):
-                y_hs[b].copy_(y_stage[b], non_blocking=True)   # host result out
-            ev_d2h[b].record(d2h_s)
-    stream.wait_stream(h2d_s)
-    stream.wait_stream(d2h_s)
-    e_b.record(stream)
-    torch.cuda.synchronize()
-    t = torch.tensor([e_a.elapsed_time(e_b)], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    def pipeline(steps):
+        """``steps`` streamed steps; returns the device time of all of them
+        (ms, max over ranks)."""
+        sync_all()
+        layer.plan.barrier()
+        e_a = torch.cuda.Event(enable_timing=True)
+        e_b = torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
+        h2d_s.wait_event(e_a)
+        d2h_s.wait_event(e_a)
+        h2d_step(0)
+        for i in range(steps):
+            b = i % 2
+            if i + 1 < steps:
+                h2d_step(i + 1)
+            stream.wait_event(ev_in[b])
+            y = runners[b]()                           # the captured forward
+            ev_free[b].record(stream)
+            if copy_out:
+                if i >= 2:
+                    stream.wait_event(ev_d2h[b])       # y_stage[b] drained to host
+                y_stage[b].copy_(y, non_blocking=True)
+                ev_out[b].record(stream)
+                d2h_s.wait_event(ev_out[b])
+                with torch.cuda.stream(d2h_s):
+                    y_hs[b].copy_(y_stage[b], non_blocking=True)   # host result out
+                ev_d2h[b].record(d2h_s)
+        stream.wait_stream(h2d_s)
+        stream.wait_stream(d2h_s)
+        e_b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e_a.elapsed_time(e_b)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    pipeline(max(3, args.warmup))        # untimed: first DMA from the pinned buffers, streams
+    t_ms = pipeline(args.steps)
     runners[1].check()
-    e2e_step = float(t.item()) / args.steps
+    e2e_step = t_ms / args.steps
     h2d = (x_h.numel() * 2 + l_h.numel() * 4) * world
     d2h = T * H * 2 * n
     return {"value": T_GLOBAL / (e2e_step / 1e3), "unit": "tokens/s",
@@ -855,8 +861,9 @@ def run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync
             "d2h_bytes_per_step": int(d2h),
             "note": "every step: pinned host x/logits copied in (H2D stream), the captured "
                     "MoELayer forward, y copied back to pinned host (D2H stream); copies of "
-                    "neighbouring steps overlap the forward (double-buffered); one timed "
-                    "region over all steps"}
+                    "neighbouring steps overlap the forward (double-buffered); W untimed "
+                    "warm-up steps of the same pipeline, then one timed region over all K "
+                    "steps"}
 
 
 LAYOUT_NOTE = ""
