@@ -919,13 +919,13 @@ def set_config(name, tokens=None):
 
 
 def reference_layout(args):
+    """(n, m) the reference arm simulates: this arm's explicit --tp, else the
+    config's named layout (the reference arm never imports the product
+    package, so --tp auto falls back to the named layout)."""
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    if args.tp == "auto" or world == 1:
-        from paper_2601_08800_b200.layer import layout_for
-        return layout_for(world, None if world == 1 else min(world, 4 if CONFIG == "C" else 2))
-    if args.tp is not None:
-        return world // int(args.tp), int(args.tp)
-    tp = min(world, 4 if CONFIG == "C" else 2)
+    if world == 1:
+        return 1, 1
+    tp = int(args.tp) if args.tp not in (None, "auto") else min(world, 4 if CONFIG == "C" else 2)
     return world // tp, tp
 
 
