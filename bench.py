@@ -7,7 +7,7 @@ Workload (``--config``):
     fp32 gate logits), TP2 x EP(N/2) -- config B's TP2xEP4 at N=8;
   C BASELINE.json configs[2], the DeepSeek-R1-shaped layer (h=7168,
     I=2048, 256 routed experts top-8 + a 2048-wide shared expert, fp8 e4m3
-    experts, DeepSeek-V3 gate), TP4 x EP(N/4) -- TP4xEP2 at N=8.
+    experts, DeepSeek-V3 gate), TP(N/2) x EP2 -- TP4xEP2 at N=8.
 One step = one full layer forward (gate top-k -> dispatch -> grouped GEMM
 -> combine) over a prefill batch of 8192 tokens; total work is fixed as N
 grows ("scaling": "strong"); pure 1x1 at N=1.  ``--tp auto`` takes the
@@ -869,9 +869,18 @@ def run_e2e(layer, runner, x, logits, args, world, tp, n, T, stream, flush, sync
 LAYOUT_NOTE = ""
 
 
+def named_tp(world):
+    """TP degree of the config's named layout family: config B TP2 x EP(N/2)
+    (TP2xEP4 at 8 GPUs), config C TP(N/2) x EP2 (TP4xEP2 at 8 GPUs; at 4
+    GPUs TP2xEP2 measured 1.76 vs 1.97 ms for TP4, profiles/r02_configC_n4_layouts.jsonl)."""
+    if world == 1:
+        return 1
+    return max(1, world // 2) if CONFIG == "C" else min(world, 2)
+
+
 def choose_layout(args, world):
     """(n, m) of the run: the config's named layout (B: TP2 x EP(N/2), C:
-    TP4 x EP(N/4), pure TP/EP below that), an explicit --tp, or --tp auto:
+    TP(N/2) x EP2, pure TP/EP below that), an explicit --tp, or --tp auto:
     the fused-layer model's first pick (layer_model.select_layout) for this
     run's own routing (every rank computes it from the same seeded logits)."""
     global LAYOUT_NOTE
@@ -888,8 +897,8 @@ def choose_layout(args, world):
     if args.tp not in (None, "auto"):
         LAYOUT_NOTE = "--tp"
         return layout_for(world, int(args.tp))
-    tp = 1 if world == 1 else min(world, 4 if CONFIG == "C" else 2)
-    LAYOUT_NOTE = f"config {CONFIG}'s named layout (TP{tp} x EP{world // tp})"
+    tp = named_tp(world)
+    LAYOUT_NOTE = f"config {CONFIG}'s named layout family (TP{tp} x EP{world // tp})"
     return layout_for(world, tp)
 
 
@@ -925,7 +934,7 @@ def reference_layout(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if world == 1:
         return 1, 1
-    tp = int(args.tp) if args.tp not in (None, "auto") else min(world, 4 if CONFIG == "C" else 2)
+    tp = int(args.tp) if args.tp not in (None, "auto") else named_tp(world)
     return world // tp, tp
 
 
