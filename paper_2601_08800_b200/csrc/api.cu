@@ -221,8 +221,6 @@ static Offsets compute_offsets(const mx_plan_desc& d, long long cap) {
   o.part_s = take(Ist ? T * h * 2 : 0);
   o.sh_meta = take(16);
   o.sub = take(4 * 5 * 2 * E);
-  o.xready = take(8 * ((size_t)cap / 128 + 2));
-  o.xcount = take(4 * ((size_t)cap / 128 + 2));
   o.total = p;
   return o;
 }
@@ -285,15 +283,6 @@ static bool gathers(const mx_plan* p) {
   const bool enabled = e && e[0] == '1';
   return enabled && p->d.expert_kind == MX_EXPERT_SWIGLU &&
          (p->d.wire == MX_WIRE_TOKEN || p->d.n_group == 1);
-}
-
-// GEMM1 expanding the token wire's XBUF rows itself (MX_FUSED_EXPAND=0
-// turns it off): bf16 SwiGLU experts with the rows written expert-major.
-static bool fused_expand(const mx_plan* p) {
-  const char* e = getenv("MX_FUSED_EXPAND");
-  if (e && e[0] == '0') return false;
-  return p->d.expert_kind == MX_EXPERT_SWIGLU && p->d.act_dtype == MX_BF16 &&
-         (p->d.hidden * 2) % 16 == 0;
 }
 
 extern "C" {
@@ -654,12 +643,9 @@ int mx_expert_stage(mx_plan* p, int rank, const mx_expert_params* ep, int stage,
     vfirst.sync_signal = 0;
     vlast.sync_wait = 0;
     if (tok) v.sync_wait = v.sync_signal = 0;
-    // fused expand: the row table only, GEMM1's idle warps copy the XBUF rows
-    // into RECV in row order while its producer waits per 128-row block
-    v.xexp = vfirst.xexp = vlast.xexp = tok && !v.a_src && fused_expand(p);
     if (tok && (stage == 0 || stage == 3)) {
       // gathered GEMM1 only needs the row table; otherwise expand into RECV
-      rc = (v.a_src || v.xexp) ? launch_rowsrc_token(vfirst, s) : launch_expand(vfirst, s);
+      rc = v.a_src ? launch_rowsrc_token(vfirst, s) : launch_expand(vfirst, s);
       if (rc) return rc;
     }
     if (stage == 3 || stage == 4) {

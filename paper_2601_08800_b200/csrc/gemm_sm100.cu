@@ -216,23 +216,6 @@ struct Args {
   const int32_t* b_index;
   int G, N, K, ldd, out_f32;
   long long M_cap;
-  // fused expand (token wire, GEMM1): warps 2-3 copy XBUF row ex_src[r] to
-  // RECV row r (rows of the other groups' pairs; own rows are in place), in
-  // row order through a global cursor; the producer waits until every
-  // 128-row block of a tile's A rows carries this forward's epoch
-  const int32_t* ex_src;
-  const char* ex_xbuf;
-  char* ex_recv;
-  unsigned long long* ex_ready;
-  int* ex_count;
-  int* ex_cursor;
-  const unsigned long long* ex_epoch;
-  int* ex_err;
-  const int* ex_rows_p;   // host_rows[group] (RECV rows of this host)
-  const int* ex_own_p;    // poff[g][g]: first own-group pair
-  const int* ex_ucnt_p;   // ucnt_all[g][g]: own-group pairs
-  long long ex_cap;
-  int ex_row_bytes;
   // clock probe: CTA 0 records {SM cycles, %globaltimer ns} over its
   // lifetime -- the effective SM clock the GEMM ran at (power capping
   // lowers it under sustained tensor load; bench.py reports it)
@@ -340,48 +323,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   const bool probe = args.clk && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long clk0 = probe ? clock64() : 0, gt0 = probe ? globaltimer_ns() : 0;
 
-  if (SWIGLU && !GATHER && !FP8 && args.ex_src && (warp == 2 || warp == 3)) {
-    // ===== fused expand: rows in ascending order, 4 per grab (a grab never
-    // straddles a 128-row block); the grab completing a block publishes the
-    // forward's epoch in ex_ready[block]
-    const unsigned long long ep = *reinterpret_cast<volatile const unsigned long long*>(args.ex_epoch);
-    const int rb = args.ex_row_bytes;
-    const int ex_rows = (int)min((long long)*args.ex_rows_p, args.ex_cap);
-    const int own0 = *args.ex_own_p, own1 = own0 + *args.ex_ucnt_p;
-    for (;;) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(args.ex_cursor, 4);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base >= ex_rows) break;
-      const int hi = base + 4 < ex_rows ? base + 4 : ex_rows;
-      for (int r = base; r < hi; ++r) {
-        const int u = args.ex_src[r];
-        if (u >= own0 && u < own1) continue;  // own rows: written by the dispatch
-        const char* src = args.ex_xbuf + (size_t)u * rb;
-        char* dst = args.ex_recv + (size_t)r * rb;
-        for (int o = lane * 16; o < rb; o += 32 * 16 * 4) {
-          uint4 val[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (o + q * 512 < rb) val[q] = ld_v4(src + o + q * 512);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (o + q * 512 < rb) st_v4(dst + o + q * 512, val[q]);
-        }
-      }
-      __threadfence();  // every lane's stores before the block count
-      __syncwarp();
-      if (lane == 0) {
-        const int b = base >> 7;
-        const int in_block = (b + 1) * 128 < ex_rows ? 128 : ex_rows - b * 128;
-        if (atomicAdd(args.ex_count + b, hi - base) + (hi - base) == in_block) {
-          __threadfence();
-          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(args.ex_ready + b), "l"(ep)
-                       : "memory");
-        }
-      }
-    }
-  } else if (warp == 0 || (GATHER && warp == 3)) {
+  if (warp == 0 || (GATHER && warp == 3)) {
     if constexpr (GATHER) {
       // ===== gathering producer (warps 0 and 3): A rows come from an
       // arbitrary row table (token rows of x / XBUF), so they are brought
@@ -450,23 +392,6 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         const int a_row = s_off[g] + mb * BM;
         const int bg = args.b_index ? args.b_index[g] : g;
         const int b_row = bg * args.N + nb * BN;
-        if (SWIGLU && !FP8 && args.ex_src) {
-          // fused expand: this tile's A rows must have been copied in
-          const unsigned long long ep =
-              *reinterpret_cast<volatile const unsigned long long*>(args.ex_epoch);
-          const int rows = s_cnt[g] - mb * BM < BM ? s_cnt[g] - mb * BM : BM;
-          const int ex_rows = (int)min((long long)*args.ex_rows_p, args.ex_cap);
-          const long long t0 = clock64();
-          for (int b = a_row >> 7; b <= (a_row + rows - 1) >> 7 && b * 128 < ex_rows; ++b) {
-            unsigned long long got;
-            do {
-              asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(got) : "l"(args.ex_ready + b)
-                           : "memory");
-              if (got != ep && clock64() - t0 > 20000000000LL) { atomicOr(args.ex_err, 1); break; }
-            } while (got != ep);
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> TMA reads
-        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -1052,23 +977,6 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   if (sync) {
     a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal;
     a.clk = at<unsigned long long>(*sync, sync->rank, sync->off.stamps) + (swiglu ? 56 : 58);
-    if (sync->xexp && swiglu && !gather) {
-      const DevView& v = *sync;
-      a.ex_src = at<int32_t>(v, v.rank, v.off.recv_src);
-      a.ex_xbuf = at<char>(v, v.rank, v.off.xbuf);
-      a.ex_recv = at<char>(v, v.rank, v.off.recv);
-      a.ex_ready = at<unsigned long long>(v, v.rank, v.off.xready);
-      a.ex_count = at<int>(v, v.rank, v.off.xcount);
-      a.ex_cursor = at<int>(v, v.rank, v.off.counters) + 12;
-      // the expand epoch: bumped by the row-table kernel before every GEMM1
-      a.ex_epoch = reinterpret_cast<const unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 14);
-      a.ex_err = at<int>(v, v.rank, v.off.err) + 2;
-      a.ex_rows_p = at<int>(v, v.rank, v.off.host_rows) + v.group;
-      a.ex_own_p = at<int>(v, v.rank, v.off.poff) + v.group * v.n + v.group;
-      a.ex_ucnt_p = at<int>(v, v.rank, v.off.ucnt_all) + v.group * v.n + v.group;
-      a.ex_cap = v.cap;
-      a.ex_row_bytes = v.wrow;
-    }
   }
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }

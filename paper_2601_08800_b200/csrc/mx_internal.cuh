@@ -82,13 +82,7 @@ struct Offsets {
   // offs/counts of the rows before and after the own sub-block (2*El), [4]
   // their local expert (GEMM b_index); stride 2*E ints
   size_t sub;
-  // fused expand (GEMM1 expands the token wire's rows itself): per 128-row
-  // block of RECV the epoch at which it was expanded, and rows done so far
-  size_t xready;      // uint64 [cap/128 + 1]
-  size_t xcount;      // int32  [cap/128 + 1]
   size_t counters;    // int32 [16]  [0]=route CTA counter [2..3]=u64 barrier epoch
-                      //   [4] grid arrivals [8..9] u64 exchange go flag [12] expand
-                      //   row cursor [14..15] u64 expand epoch
   size_t err;         // int32 [16]  [0]=capacity [1]=bad id [2]=timeout
   size_t stamps;      // uint64 [MX_STAMPS] %globaltimer ns written by mx_stamp
   size_t total;
@@ -111,7 +105,6 @@ struct DevView {
   int Is_t;           // shared expert intermediate per TP rank (0: none)
   int sync_signal;    // fused barrier: this kernel's last CTA publishes the epoch
   int sync_wait;      // fused barrier: every CTA waits for all peers' epoch at entry
-  int xexp;           // token wire: GEMM1 expands the XBUF rows into RECV itself
   const void* a_src;  // GEMM1 gathers A rows from here (x or XBUF), nullptr: RECV
   long long a_src_rows;
   long long cap;

@@ -781,16 +781,6 @@ __global__ void k_rowsrc_token(DevView v) {
     const int i = (int)(q % v.KH);
     if (i < pn[u] && pe[q].p < v.cap) src[pe[q].p] = (int)u;
   }
-  if (v.xexp) {  // fused expand: fresh row cursor, per-block row counts and epoch
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      at<int>(v, v.rank, v.off.counters)[12] = 0;
-      ++*reinterpret_cast<unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 14);
-    }
-    int* cnt = at<int>(v, v.rank, v.off.xcount);
-    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < v.cap / 128 + 1;
-         b += (long long)gridDim.x * blockDim.x)
-      cnt[b] = 0;
-  }
 }
 
 static int blocks_for(long long warps) {
