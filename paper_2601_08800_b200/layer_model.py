@@ -36,19 +36,25 @@ __all__ = ["LayerCalibration", "routing_stats", "predict_layer", "select_layout"
 
 @dataclass(frozen=True)
 class LayerCalibration:
-    """Peaks (MEASURED_PEAKS.json / B200_PROFILING.md) and per-phase
-    efficiencies; defaults are the round-1 B200 measurements
-    (profiles/r01_n{1,2,4}_bench.json ``rooflines``)."""
+    """Peaks and per-phase efficiencies (achieved / peak).  Only their
+    product -- the phase's measured throughput -- enters a prediction.  The
+    defaults are the round-1 B200 measurements (profiles/r01_n{1,2,4}_bench.json
+    ``rooflines``) expressed against the round-2 denominators bench.py
+    divides by: MEASURED_PEAKS.json's HBM copy (6446.3 GB/s) and burst bf16
+    matmul (1668.3 TF/s), and the same-run NVLink probe at 4 GPUs (651 GB/s,
+    profiles/r02_n4_tp2_bench.json); ``from_bench`` re-derives them from
+    newer lines."""
 
-    hbm_gbs: float = 6539.5
-    nvlink_gbs: float = 770.0
-    bf16_tflops: float = 1397.3
+    hbm_gbs: float = 6446.3
+    nvlink_gbs: float = 651.0
+    bf16_tflops: float = 1668.3
     # GEMM efficiency vs the TP shard I/m: {I/m: (gemm1, gemm2)}
-    gemm_eff: dict = field(default_factory=lambda: {384: (0.67, 0.60), 768: (0.83, 0.73)})
+    gemm_eff: dict = field(default_factory=lambda: {384: (0.5612, 0.5025),
+                                                    768: (0.6952, 0.6114)})
     eff: dict = field(default_factory=lambda: {
-        "dispatch_nvlink": 0.59, "dispatch_hbm": 0.86, "expand": 0.70,
-        "pair_reduce": 0.60, "pair_push_nvlink": 0.49, "combine_nvlink": 0.40,
-        "combine_hbm": 0.63})
+        "dispatch_nvlink": 0.6978, "dispatch_hbm": 0.8724, "expand": 0.7101,
+        "pair_reduce": 0.6087, "pair_push_nvlink": 0.5796, "combine_nvlink": 0.4731,
+        "combine_hbm": 0.6391})
     route_layout_us: float = 32.0
     barrier_us: float = 6.0   # graph replay: ~5 us intrinsic (barrier_bench) + skew
 
