@@ -350,10 +350,30 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
     }
     for (int d = 0; d < n; ++d) tok_pair_rank[(size_t)(t0 + tl) * n + d] = s_hp[tl * n + d];
   }
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    chunk_hist[e * v.C + c] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
-                              __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
+  if (v.C > 1) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      chunk_hist[e * v.C + c] = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
+                                __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
+    }
+    return;
   }
+  // one chunk (decode-sized groups): the chunk scans of k_route_scan are
+  // trivial -- every exclusive prefix is 0 and the totals are this CTA's
+  // counts -- so they are done here and the scan kernel is not launched
+  __syncthreads();  // chunk_host / chunk_pair of this chunk are written above
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int tot = __popc(s_mask[e * 4]) + __popc(s_mask[e * 4 + 1]) +
+                    __popc(s_mask[e * 4 + 2]) + __popc(s_mask[e * 4 + 3]);
+    chunk_hist[e] = 0;
+    for (int r = 0; r < v.W; ++r) at<int>(v, r, v.off.cnt_all)[v.group * E + e] = tot;
+  }
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    const int u = chunk_pair[d];
+    chunk_host[d] = 0;
+    chunk_pair[d] = 0;
+    for (int r = 0; r < v.W; ++r) at<int>(v, r, v.off.ucnt_all)[v.group * n + d] = u;
+  }
+  if (v.sync_signal) grid_signal(v);  // counts published: barrier #1
 }
 
 // Exclusive prefix of the chunk counts, one warp per expert (and per host),
@@ -599,6 +619,7 @@ int launch_route(const DevView& v, const float* logits, const int32_t* ids,
   int rc = v.elt == 8 ? launch_route_wt<double>(v, C, smem, logits, ids, w, s)
                       : launch_route_wt<float>(v, C, smem, logits, ids, w, s);
   if (rc) return rc;
+  if (C == 1) return MX_OK;  // k_route did the (trivial) scans itself
   const int warps = v.E + 2 * v.n;
   pdl_launch(k_route_scan, (warps + 7) / 8, 256, 0, s, v);
   MX_LAUNCH_CHECK();
