@@ -1164,16 +1164,22 @@ static int launch_astat(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
                         const Args& a, cudaStream_t s) {
   using C = Cfg<256>;
   auto kern = k_grouped_gemm_astat<256>;
+  static int static_smem = -1;
+  if (static_smem < 0) {
+    cudaFuncAttributes fa{};
+    MX_CUDA(cudaFuncGetAttributes(&fa, kern));
+    static_smem = (int)fa.sharedSizeBytes;
+  }
   const int kblocks = a.K / BK;
-  const int budget = 227 * 1024 - 1024 /*align*/ - 1024 /*barriers*/ - C::STAGING;
+  const int budget = 227 * 1024 - static_smem - 1024 /*align*/ - 1024 /*barriers*/ - C::STAGING;
   int nstages = (budget - kblocks * C::A_BYTES) / C::B_BYTES;
   if (nstages > 4) nstages = 4;
   if (nstages < 2) { set_error("A-stationary GEMM: K too large"); return MX_ERR_UNSUPPORTED; }
   const int smem = kblocks * C::A_BYTES + nstages * C::B_BYTES + 1024 + 1024 + C::STAGING;
-  static bool attr = false;
-  if (!attr) {
-    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
+  static int attr = 0;
+  if (attr < smem) {
+    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
   }
   pdl_launch(kern, gemm_ctas(), NUM_THREADS_1, smem, s, ma, mb, md, a, nstages);
   MX_LAUNCH_CHECK();
