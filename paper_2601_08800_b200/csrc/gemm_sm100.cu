@@ -555,256 +555,6 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   if (args.sync_signal) grid_signal(args.sv);  // D complete (bulk stores drained): publish
 }
 
-// ------------------------------------------------------------ short K: A-stationary
-// GEMM2 at the TP layouts has K = I/m <= 384: a tile is only 6 k-blocks, and
-// the MMA warp waits for the first stage of every new tile (fresh rows and a
-// new weight panel, ncu: profiles/r02_ncu_summary.txt) -- 0.51 of the burst
-// peak at TP2 x EP2.  Here a work item is (expert, 128-row block, a run of
-// n-blocks): its whole A block (K x 128 rows, <= 96 KB) is loaded once into
-// shared memory and stays there while the B panels of the item's n-blocks
-// stream through a ring behind it, so the tensor pipe sees one A load per
-// item instead of one per tile and the B stream never restarts.
-// Accumulators double-buffered in TMEM as in k_grouped_gemm; bf16 output,
-// no SwiGLU (GEMM2 only).  The item count is set on the device from the
-// routed rows (n-block runs split until there are ~3 items per CTA).
-constexpr int AS_KB_MAX = 6;   // K <= 384
-template <int BN>
-__global__ void __launch_bounds__(NUM_THREADS_1, 1)
-k_grouped_gemm_astat(const __grid_constant__ CUtensorMap map_a,
-                     const __grid_constant__ CUtensorMap map_b,
-                     const __grid_constant__ CUtensorMap map_d, Args args, int nstages) {
-  using C = Cfg<BN>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int kblocks = args.K / BK;
-  unsigned char* sA = smem;                                   // kblocks x 16 KB
-  unsigned char* sB = smem + kblocks * C::A_BYTES;            // nstages x B_BYTES
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + nstages * C::B_BYTES);
-  uint64_t* empty = full + nstages;
-  uint64_t* tfull = empty + nstages;  // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint64_t* afull = tempty + 2;
-  uint64_t* aempty = afull + 1;
-  unsigned char* staging = reinterpret_cast<unsigned char*>(full) + 1024;
-  __shared__ uint32_t s_tmem;
-  __shared__ int s_tstart[MX_EMAX + 1];
-  __shared__ int s_off[MX_EMAX];
-  __shared__ int s_cnt[MX_EMAX];
-  __shared__ int s_split;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = args.G, nN = args.N / BN;
-  pdl_wait();
-  if (args.sync_wait) grid_wait(args.sv);
-  for (int g = threadIdx.x; g < G; g += blockDim.x) {
-    s_off[g] = args.offs[g];
-    s_cnt[g] = args.cnts[g];
-  }
-  __syncthreads();
-  if (warp == 3) {
-    // row blocks per group, then the n-block split that gives ~3 items per
-    // CTA (every CTA computes the same value), then the item prefix
-    int carry = 0;
-    for (int base = 0; base < G; base += 32) {
-      const int g = base + lane;
-      int rb = g < G ? (s_cnt[g] + BM - 1) / BM : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rb += __shfl_xor_sync(0xffffffffu, rb, o);
-      carry += rb;
-    }
-    int split = carry > 0 ? (3 * (int)gridDim.x + carry - 1) / carry : 1;
-    split = split < 1 ? 1 : (split > nN ? nN : split);
-    carry = 0;
-    for (int base = 0; base < G; base += 32) {
-      const int g = base + lane;
-      const int items = g < G ? ((s_cnt[g] + BM - 1) / BM) * split : 0;
-      int incl = items;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (g < G) s_tstart[g] = carry + incl - items;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) { s_tstart[G] = carry; s_split = split; }
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&map_a);
-    tma_prefetch(&map_b);
-    tma_prefetch(&map_d);
-  }
-  if (warp == 1 && lane == 0) {
-    for (int st = 0; st < nstages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
-    }
-    mbar_init(afull, 1);
-    mbar_init(aempty, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&s_tmem)),
-                 "r"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = s_tmem;
-  const int total_items = s_tstart[G];
-  const int split = s_split;
-  const bool probe = args.clk && blockIdx.x == 0 && threadIdx.x == 0;
-  const unsigned long long clk0 = probe ? clock64() : 0, gt0 = probe ? globaltimer_ns() : 0;
-  // item -> (group, row block, n-block run [n0, n1))
-  auto decode_item = [&](int t, int* g, int* mb, int* n0, int* n1) {
-    int lo = 0, hi = G - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_tstart[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    const int r = t - s_tstart[lo];
-    *g = lo;
-    *mb = r / split;
-    const int sp = r % split;
-    *n0 = sp * nN / split;
-    *n1 = (sp + 1) * nN / split;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer: the item's A block once, then its B panels
-      int stage = 0;
-      uint32_t phase = 0, aphase = 0;
-      for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-        int g, mb, n0, n1;
-        decode_item(t, &g, &mb, &n0, &n1);
-        const int a_row = s_off[g] + mb * BM;
-        const int bg = args.b_index ? args.b_index[g] : g;
-        mbar_wait(aempty, aphase ^ 1);  // the previous item's MMAs are done with A
-        mbar_expect_tx(afull, kblocks * C::A_BYTES);
-        for (int kb = 0; kb < kblocks; ++kb)
-          tma_load_2d(sA + kb * C::A_BYTES, &map_a, afull, kb * BK, a_row);
-        aphase ^= 1;
-        for (int nb = n0; nb < n1; ++nb) {
-          const int b_row = bg * args.N + nb * BN;
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], C::B_BYTES);
-            tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * BK, b_row);
-            if (++stage == nstages) { stage = 0; phase ^= 1; }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer
-      constexpr uint32_t idesc = idesc_bf16<BN>();
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0, aphase = 0;
-      for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-        int g, mb, n0, n1;
-        decode_item(t, &g, &mb, &n0, &n1);
-        mbar_wait(afull, aphase);
-        aphase ^= 1;
-        tc_fence_after();
-        for (int nb = n0; nb < n1; ++nb) {
-          mbar_wait(&tempty[acc], acc_phase ^ 1);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem + acc * BN;
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint64_t adesc = smem_desc_sw128(smem_u32(sA + kb * C::A_BYTES));
-            const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(d_tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kb | kk) != 0);
-            mma_commit(&empty[stage]);
-            if (++stage == nstages) { stage = 0; phase ^= 1; }
-          }
-          mma_commit(&tfull[acc]);
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-        mma_commit(aempty);  // A free once this item's MMAs retire
-      }
-    }
-  } else if (warp >= 4) {
-    // ===== epilogue (bf16): as k_grouped_gemm, tile = (group, row block, n-block)
-    const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    const int row_in_tile = q * 32 + lane;
-    unsigned char* my_stage = staging + (warp - 4) * (32 * 64);
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_items; t += gridDim.x) {
-      int g, mb, n0, n1;
-      decode_item(t, &g, &mb, &n0, &n1);
-      const int cnt = s_cnt[g];
-      const int r_local = mb * BM + row_in_tile;
-      const long long row = (long long)s_off[g] + r_local;
-      const bool valid = r_local < cnt && row < args.M_cap;
-      const bool full_box = (mb * BM + q * 32 + 31) < cnt;
-      const int row0 = s_off[g] + mb * BM + q * 32;
-      for (int nb = n0; nb < n1; ++nb) {
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
-#pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c, r);
-          tmem_wait_ld();
-          uint32_t packed[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 b2 =
-                __floats2bfloat162_rn(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-            packed[i] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          if (full_box) {
-            stage_store_chunk<0>(my_stage, packed, lane, &map_d, nb * BN + c, row0);
-          } else if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.D) +
-                                                  row * args.ldd + nb * BN + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-    if (lane == 0) {
-      tma_store_wait_all();
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (probe) {
-    args.clk[0] = clock64() - clk0;
-    args.clk[1] = globaltimer_ns() - gt0;
-  }
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(C::TMEM_COLS));
-  }
-  if (args.sync_signal) grid_signal(args.sv);
-}
-
 // ------------------------------------------------------------ CTA pair (2SM)
 // tcgen05.mma.cta_group::2, M=256 x N=256 tiles: CTA rank c of the cluster
 // pair loads A rows [c*128, c*128+128) and B rows [c*128, c*128+128) of the
@@ -1158,44 +908,6 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   return MX_OK;
 }
 
-// A-stationary short-K kernel: stages of the B ring from what the A block
-// leaves of shared memory (<= 4)
-static int launch_astat(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
-                        const Args& a, cudaStream_t s) {
-  using C = Cfg<256>;
-  auto kern = k_grouped_gemm_astat<256>;
-  static int static_smem = -1;
-  if (static_smem < 0) {
-    cudaFuncAttributes fa{};
-    MX_CUDA(cudaFuncGetAttributes(&fa, kern));
-    static_smem = (int)fa.sharedSizeBytes;
-  }
-  const int kblocks = a.K / BK;
-  const int budget = 227 * 1024 - static_smem - 1024 /*align*/ - 1024 /*barriers*/ - C::STAGING;
-  int nstages = (budget - kblocks * C::A_BYTES) / C::B_BYTES;
-  if (nstages > 4) nstages = 4;
-  if (nstages < 2) { set_error("A-stationary GEMM: K too large"); return MX_ERR_UNSUPPORTED; }
-  const int smem = kblocks * C::A_BYTES + nstages * C::B_BYTES + 1024 + 1024 + C::STAGING;
-  static int attr = 0;
-  if (attr < smem) {
-    MX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = smem;
-  }
-  pdl_launch(kern, gemm_ctas(), NUM_THREADS_1, smem, s, ma, mb, md, a, nstages);
-  MX_LAUNCH_CHECK();
-  return MX_OK;
-}
-
-// 1 (default): GEMMs with K <= 384, bf16 out, no SwiGLU take the
-// A-stationary kernel; 0: never (MX_GEMM_ASTAT)
-static bool use_astat(int K, int swiglu, int out_dtype, bool gather) {
-  static const int v = [] {
-    const char* e = getenv("MX_GEMM_ASTAT");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0 && !swiglu && !gather && out_dtype == MX_BF16 && K / BK <= AS_KB_MAX;
-}
-
 template <bool SWIGLU>
 static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                        const Args& a, long long max_tiles, cudaStream_t s) {
@@ -1277,11 +989,6 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
                                  : launch<256, false, true>(ma, mb, md, a, max_tiles, s);
     return swiglu ? launch<128, true, true>(ma, mb, md, a, max_tiles, s)
                   : launch<128, false, true>(ma, mb, md, a, max_tiles, s);
-  }
-  if (N % 256 == 0 && use_astat(K, swiglu, out_dtype, gather)) {
-    CUtensorMap mb256;   // B boxes of 256 rows whatever bn the tile picker chose
-    if (bn != 256 && (rc = make_map(&mb256, B, b_rows, K, 256))) return rc;
-    return launch_astat(ma, bn == 256 ? mb : mb256, md, a, s);
   }
   if (bn == 256 && out_dtype == MX_BF16 && use_pair(G, M_total)) {
     // CTA-pair kernel: A box 128 rows (each CTA its half of the 256-row tile),
