@@ -96,3 +96,44 @@ def test_config_c_model_counts_the_shared_expert_and_fp8_rows():
     finally:
         bench.set_config("B")
     assert bench.WROW == bench.H * 2 == 4096
+
+
+def test_named_layouts_and_reference_layout():
+    """The bench's default layouts (BASELINE's named layouts at 8 GPUs: config
+    B TP2 x EP4, config C TP4 x EP2) and the reference arm's layout, which
+    must not import the product package."""
+    import os
+
+    class A:
+        tp = None
+        gpus = 8
+
+    try:
+        for cfg, want in (("B", [1, 2, 2, 2]), ("C", [1, 1, 2, 4])):
+            bench.set_config(cfg)
+            assert [bench.named_tp(w) for w in (1, 2, 4, 8)] == want
+        old = os.environ.get("WORLD_SIZE")
+        os.environ["WORLD_SIZE"] = "8"
+        bench.set_config("B")
+        assert bench.reference_layout(A()) == (4, 2)
+        bench.set_config("C")
+        assert bench.reference_layout(A()) == (2, 4)
+        A.tp = "1"
+        assert bench.reference_layout(A()) == (8, 1)
+        A.tp = "auto"                                  # falls back to the named layout
+        assert bench.reference_layout(A()) == (2, 4)
+    finally:
+        bench.set_config("B")
+        if old is None:
+            os.environ.pop("WORLD_SIZE", None)
+        else:
+            os.environ["WORLD_SIZE"] = old
+
+
+def test_gemm_clock_and_fp8_peak_helpers_exist():
+    """bench.py reports the GEMMs' SM clock from the stamp slots the kernels
+    write (56-63) and measures the fp8 peak in the run for config C."""
+    import inspect
+    src = inspect.getsource(bench.gemm_clocks)
+    assert "56:64" in src
+    assert callable(bench.measure_fp8_peak) and callable(bench.nvlink_probe)

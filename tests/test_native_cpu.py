@@ -116,3 +116,29 @@ def test_nvlink_diagnostic_kernels_build_for_sm100a():
                    check=True, capture_output=True)
     lib = C.CDLL(str(out))
     assert hasattr(lib, "nb_launch") and hasattr(lib, "nb_enable_peers")
+
+
+def test_plan_input_validation_messages():
+    """LayerPlan._on_device / _routing_inputs reject what the C ABI would
+    misread (shape, dtype of hidden states, both or neither routing input)
+    with StrategyError -- checked without a GPU through a stand-in plan."""
+    import pytest
+    import torch
+    from paper_2601_08800_b200.errors import StrategyError
+    from paper_2601_08800_b200.plan import LayerPlan
+
+    p = LayerPlan.__new__(LayerPlan)
+    p.emulate, p.n, p.tokens, p.hidden, p.num_experts, p.top_k = False, 1, 4, 8, 16, 2
+    p.dtype, p.wdtype, p.device = torch.bfloat16, torch.float32, torch.device("cpu")
+    x = torch.zeros(4, 8, dtype=torch.bfloat16)
+    assert p._on_device(x, "x", torch.bfloat16, 8, False) is not None
+    with pytest.raises(StrategyError, match="shape"):
+        p._on_device(torch.zeros(3, 8, dtype=torch.bfloat16), "x", torch.bfloat16, 8, False)
+    with pytest.raises(StrategyError, match="dtype"):
+        p._on_device(x.float(), "x", torch.bfloat16, 8, False)
+    ids = torch.zeros(4, 2, dtype=torch.int64)          # torch.topk indices
+    assert p._on_device(ids, "ids", torch.int32, 2, True).dtype == torch.int32
+    with pytest.raises(StrategyError, match="exactly one"):
+        p._routing_inputs(None, None, None)
+    with pytest.raises(StrategyError, match="weights"):
+        p._routing_inputs(None, ids, None)
