@@ -878,21 +878,32 @@ def named_tp(world):
     return max(1, world // 2) if CONFIG == "C" else min(world, 2)
 
 
+def auto_default(world):
+    """Config B at 2 and 4 GPUs, where BASELINE.json names no layout: the
+    fused-layer model's pick (the strategy selection the layer is built
+    around) instead of extrapolating the 8-GPU TP2 x EP4."""
+    return CONFIG == "B" and world in (2, 4)
+
+
 def choose_layout(args, world):
-    """(n, m) of the run: the config's named layout (B: TP2 x EP(N/2), C:
-    TP(N/2) x EP2, pure TP/EP below that), an explicit --tp, or --tp auto:
-    the fused-layer model's first pick (layer_model.select_layout) for this
-    run's own routing (every rank computes it from the same seeded logits)."""
+    """(n, m) of the run: an explicit --tp; --tp auto (and, by default, config
+    B at 2 and 4 GPUs): the fused-layer model's first pick
+    (layer_model.select_layout) for this run's own routing (every rank
+    computes it from the same seeded logits); otherwise the config's named
+    layout family (B: TP2 x EP(N/2) -- TP2xEP4 at 8 GPUs; C: TP(N/2) x EP2 --
+    TP4xEP2 at 8 GPUs; pure TP/EP below that)."""
     global LAYOUT_NOTE
     from paper_2601_08800_b200.layer import layout_for
-    if args.tp == "auto" and world > 1:
+    if (args.tp == "auto" or (args.tp is None and auto_default(world))) and world > 1:
         import torch
         logits = torch.cat([torch.randn(T_GLOBAL // world, E, device="cuda",
                                         generator=torch.Generator(device="cuda").manual_seed(
                                             2000 + r)) for r in range(world)])
         ids = torch.topk(logits, K_TOP, dim=-1).indices.cpu().numpy()
         n, m = layout_for(world, "auto", routing=ids, num_experts=E, hidden=H, inter=INTER)
-        LAYOUT_NOTE = "auto: layer_model.select_layout on a routing sample of this workload"
+        LAYOUT_NOTE = ("auto: layer_model.select_layout on a routing sample of this workload"
+                       + ("" if args.tp == "auto" else
+                          " (default where BASELINE names no layout; TP2xEP4 at 8 GPUs)"))
         return n, m
     if args.tp not in (None, "auto"):
         LAYOUT_NOTE = "--tp"
@@ -929,11 +940,14 @@ def set_config(name, tokens=None):
 
 def reference_layout(args):
     """(n, m) the reference arm simulates: this arm's explicit --tp, else the
-    config's named layout (the reference arm never imports the product
-    package, so --tp auto falls back to the named layout)."""
+    config's named layout; where our arm defaults to the model's pick
+    (config B at 2 / 4 GPUs) the EP-only layout it takes on the uniform
+    router (the reference arm never imports the product package to ask)."""
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if world == 1:
         return 1, 1
+    if args.tp is None and auto_default(world):
+        return world, 1
     tp = int(args.tp) if args.tp not in (None, "auto") else named_tp(world)
     return world // tp, tp
 

@@ -115,7 +115,10 @@ def test_named_layouts_and_reference_layout():
         old = os.environ.get("WORLD_SIZE")
         os.environ["WORLD_SIZE"] = "8"
         bench.set_config("B")
-        assert bench.reference_layout(A()) == (4, 2)
+        assert bench.reference_layout(A()) == (4, 2)          # named TP2 x EP4 at 8 GPUs
+        os.environ["WORLD_SIZE"] = "4"
+        assert bench.reference_layout(A()) == (4, 1)          # the auto default's EP4
+        os.environ["WORLD_SIZE"] = "8"
         bench.set_config("C")
         assert bench.reference_layout(A()) == (2, 4)
         A.tp = "1"
