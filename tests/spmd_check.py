@@ -54,6 +54,10 @@ def gather_rows(y, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tp", type=int, default=None)
+    ap.add_argument("--bench-shape", action="store_true",
+                    help="also run config B at bench.py's dimensions (8192 tokens, h=2048, "
+                         "I=768, 128 experts top-8, token wire) in this layout and check a "
+                         "token sample against the CPU oracle")
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 as a separate process: gloo for the "
                          "bootstrap, the layer's CUDA IPC heaps, device barriers and "
@@ -214,6 +218,35 @@ def main():
                 if fro > 1e-2 or mx > 5e-2:
                     failures.append(f"fp8 {wire} rank {r}: fro {fro:.3e} max {mx:.3e}")
         print(f"fp8 layer checked over slot/token wires", flush=True)
+
+    # ---------------- config B at the bench's dimensions in this layout
+    if args.bench_shape:
+        Tg, hb, Eb, kb, Ib = 8192, 2048, 128, 8, 768
+        Tb = Tg // n
+        exb = SwiGLUExperts.random(Eb, hb, Ib, seed=0)
+        w13, w2 = exb.rank_shard(n, m, rank)
+        genb = torch.Generator(device="cuda").manual_seed(77)
+        xb = torch.randn(Tg, hb, device="cuda", generator=genb).to(torch.bfloat16)
+        lb = torch.randn(Tg, Eb, device="cuda", generator=genb)
+        big = MoELayer(n, m, Tb, hb, Eb, kb, Ib, w13=w13, w2=w2, rank=rank, wire="token")
+        yb = fwd(big, xb[g * Tb:(g + 1) * Tb].contiguous(), lb[g * Tb:(g + 1) * Tb].contiguous())
+        ybs = gather_rows(yb.clone(), world)
+        big.close()
+        del w13, w2
+        if rank == 0:
+            oexb = orc.SwiGLUOracle(exb.w_gate.float().cpu().numpy(), exb.w_up.float().cpu().numpy(),
+                                    exb.w_down.float().cpu().numpy())
+            samp = np.sort(np.random.default_rng(3).choice(Tg, 512, replace=False))
+            idsb, wb = orc.router_topk(lb.cpu().numpy()[samp], kb)
+            y_refb = orc.moe_layer_swiglu(xb.float().cpu().numpy()[samp], idsb, wb, oexb)
+            got = torch.cat([ybs[j * m] for j in range(n)]).float().cpu().numpy()[samp]
+            eb = orc.verify_metric(got, y_refb)
+            print(f"config B bench shape ({n}x{m}, 8192 tokens): err {eb:.3e} on 512 sampled tokens",
+                  flush=True)
+            if eb > 2e-2:
+                failures.append(f"config B bench shape: err {eb:.3e}")
+        del exb
+        torch.cuda.empty_cache()
 
     # ---------------- capacity below the routed rows: every rank raises
     from paper_2601_08800_b200 import CapacityError

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _run(nproc, tp=None, env=None, port_off=0, same_device=False):
+def _run(nproc, tp=None, env=None, port_off=0, same_device=False, extra=()):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
            f"--master-port={29500 + nproc * 7 + (tp or 0) + port_off}",
@@ -30,6 +30,7 @@ def _run(nproc, tp=None, env=None, port_off=0, same_device=False):
         cmd += ["--tp", str(tp)]
     if same_device:
         cmd += ["--same-device"]
+    cmd += list(extra)
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
                        env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
@@ -61,3 +62,24 @@ def test_spmd_layer_fused_barriers(nproc, tp):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     _run(nproc, tp, env={"MX_FUSE_BARRIER_T": "4096"}, port_off=50)
+
+
+def test_spmd_bench_shape_one_device():
+    """Config B at bench.py's dimensions in the EP2 layout bench.py runs at
+    2 GPUs, as two processes on cuda:0: a 512-token sample of the output
+    against the CPU oracle."""
+    if torch.cuda.device_count() < 1:
+        pytest.skip("needs a GPU")
+    out = _run(2, 1, port_off=130, same_device=True, extra=["--bench-shape"])
+    assert "config B bench shape" in out
+    print(out[-1500:])
+
+
+@pytest.mark.parametrize("nproc,tp", [(2, 1), (4, 1), (4, 2)])
+def test_spmd_bench_shape(nproc, tp):
+    """Config B at bench.py's dimensions in the 2/4-GPU layouts, one rank per
+    GPU (device barriers, NVLink)."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    out = _run(nproc, tp, port_off=160, extra=["--bench-shape"])
+    assert "config B bench shape" in out
