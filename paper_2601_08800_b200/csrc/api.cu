@@ -64,6 +64,40 @@ __global__ void k_barrier(DevView v, int r0, int nr) {
   __threadfence_system();
 }
 
+// Lean form (default): the flag store's release.sys is the one fence
+// (release is cumulative over everything the previous kernels wrote, local
+// and remote, since they happen-before this kernel), and the acquire loads
+// need no trailing fence -- later kernels are ordered after this one.
+// tools/barrier_probe.py at 2 GPUs: 3.2 vs 5.1 us per barrier (graph
+// replay, kernel boundary 0.46 us).  MX_BARRIER=0 selects k_barrier above.
+__global__ void k_barrier_lean(DevView v, int r0, int nr) {
+  pdl_wait();  // predecessor's outputs are visible after this
+  unsigned long long* ctr =
+      reinterpret_cast<unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 2);
+  const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(ctr) + 1;
+  const int r = r0 + threadIdx.x;
+  if (threadIdx.x == 0) *ctr = epoch;
+  if ((int)threadIdx.x < nr) {
+    st_release_sys(at<unsigned long long>(v, r, v.off.flags) + v.rank, epoch);
+    const unsigned long long* mine = at<unsigned long long>(v, v.rank, v.off.flags) + r;
+    long long t0 = clock64();
+    while (ld_acquire_sys(mine) < epoch) {
+      if (clock64() - t0 > (long long)20000000000LL) {  // ~10 s at 2 GHz
+        atomicOr(at<int>(v, v.rank, v.off.err) + 2, 1);
+        break;
+      }
+    }
+  }
+}
+
+static bool barrier_lean() {
+  static const bool b = [] {
+    const char* e = getenv("MX_BARRIER");
+    return !(e && e[0] == '0');
+  }();
+  return b;
+}
+
 // The barrier split in halves that never spin, for ranks that share ONE GPU
 // as separate processes (tests): nothing guarantees that kernels of
 // different processes run at the same time on one GPU, so a rank spinning
@@ -97,7 +131,8 @@ __global__ void k_barrier_verify(DevView v, int r0, int nr) {
 
 int launch_barrier(const DevView& v, cudaStream_t s, bool group_only) {
   const int r0 = group_only ? v.group * v.m : 0, nr = group_only ? v.m : v.W;
-  pdl_launch(k_barrier, 1, 64, 0, s, v, r0, nr);
+  if (barrier_lean()) pdl_launch(k_barrier_lean, 1, (nr + 31) / 32 * 32, 0, s, v, r0, nr);
+  else pdl_launch(k_barrier, 1, 64, 0, s, v, r0, nr);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }

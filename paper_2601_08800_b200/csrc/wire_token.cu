@@ -303,16 +303,24 @@ struct PairRange {
   }
 };
 
+// S warps per pair (column split, a power of two dividing the warps per
+// CTA): sub-warp s takes every S-th 32-vector column chunk, so a decode
+// batch's few pairs keep all their loads in flight at once instead of
+// walking the row in a chain of dependent rounds (same arithmetic per
+// column, same bits).
 template <int DT, class WT>
-__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v, int part) {
+__global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v, int part, int S) {
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
   constexpr int KU = 8;
   const int lane = threadIdx.x & 31;
-  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long gw0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int sub = (int)(gw0 % S);
+  const long long gw = gw0 / S;
+  const long long nwarps = (((long long)gridDim.x * blockDim.x) >> 5) / S;
+  const int cstep = S * 32 * V;
   const PairRange pr(v, part);
   const int* pn = at<int>(v, v.rank, v.off.pair_n);
   const PairEnt<WT>* pe = reinterpret_cast<const PairEnt<WT>*>(at<char>(v, v.rank, v.off.pair_p));
@@ -332,15 +340,15 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v, int part) {
       rp[i] = prt + (size_t)(ok ? e.p : 0) * h;
       w[i] = ok ? (A)e.w : (A)0;
     }
-    int c = lane * V;
+    int c = (sub * 32 + lane) * V;
     if (cnt <= KU) {
-      for (; c + 32 * V < h; c += 64 * V) {  // two column vectors per lane: 2 x cnt loads in flight
+      for (; c + cstep < h; c += 2 * cstep) {  // two column vectors per lane: 2 x cnt loads in flight
         uint4 raw[2][KU];
 #pragma unroll
         for (int i = 0; i < KU; ++i)
           if (i < cnt) {
             raw[0][i] = ld_v4(rp[i] + c);
-            raw[1][i] = ld_v4(rp[i] + c + 32 * V);
+            raw[1][i] = ld_v4(rp[i] + c + cstep);
           }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -362,11 +370,11 @@ __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v, int part) {
           T out[V];
 #pragma unroll
           for (int q = 0; q < V; ++q) out[q] = from_acc<T>(acc[q]);
-          st_v4(zin_dst<T>(v, tok, c + hh * 32 * V, sw), *reinterpret_cast<uint4*>(out));
+          st_v4(zin_dst<T>(v, tok, c + hh * cstep, sw), *reinterpret_cast<uint4*>(out));
         }
       }
     }
-    for (; c < h; c += 32 * V) {
+    for (; c < h; c += cstep) {
       A acc[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) acc[q] = (A)0;
@@ -590,15 +598,19 @@ __global__ void __launch_bounds__(PRB_WARPS * 32, 1) k_pair_reduce_bulk(DevView 
 // Owner (j, t): y[tok, cols t] = sum over host TP ranks (ascending) and hosts
 // (j-1, ..., j) of the pre-reduced partials the hosts pushed into this rank's
 // ZIN; then push the shard to every TP rank of the group (final all-gather).
+// S warps per token (column split, as in k_pair_reduce).
 template <int DT>
-__device__ __forceinline__ void combine_token_body(const DevView& v) {
+__device__ __forceinline__ void combine_token_body(const DevView& v, int S = 1) {
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
   constexpr int V = Elt<DT>::V;
   constexpr int HMAX = 8;
   const int lane = threadIdx.x & 31;
-  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long gw0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int sub = (int)(gw0 % S);
+  const long long gw = gw0 / S;
+  const long long nwarps = (((long long)gridDim.x * blockDim.x) >> 5) / S;
+  const int cstep = S * 32 * V;
   const int n = v.n, m = v.m, h = v.h, j = v.group;
   const int* upos = at<int>(v, v.rank, v.off.upos);
   int c0, c1;
@@ -623,7 +635,7 @@ __device__ __forceinline__ void combine_token_body(const DevView& v) {
         bits &= bits - 1;
       }
     }
-    int c = c0 + lane * V;
+    int c = c0 + (sub * 32 + lane) * V;
     if (m * nh <= 4) {
       // fast path: every (host TP rank, host) ZIN load of CG column
       // vectors is issued before any is consumed; the sum keeps the
@@ -639,13 +651,13 @@ __device__ __forceinline__ void combine_token_body(const DevView& v) {
         src[i] = i < m * nh ? zin + (((size_t)ha * m + tt) * v.T + t) * sw : nullptr;
       }
       constexpr int CG = 2;
-      for (; c + (CG - 1) * 32 * V < c1; c += CG * 32 * V) {
+      for (; c + (CG - 1) * cstep < c1; c += CG * cstep) {
         uint4 r[4][CG];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (i < m * nh)
 #pragma unroll
-            for (int g = 0; g < CG; ++g) r[i][g] = ld_v4(src[i] + c + g * 32 * V);
+            for (int g = 0; g < CG; ++g) r[i][g] = ld_v4(src[i] + c + g * cstep);
 #pragma unroll
         for (int g = 0; g < CG; ++g) {
           A acc[V];
@@ -658,7 +670,7 @@ __device__ __forceinline__ void combine_token_body(const DevView& v) {
 #pragma unroll
               for (int q = 0; q < V; ++q) acc[q] = add_rn(acc[q], to_acc(pv[q]));
             }
-          const int cg = c + g * 32 * V;
+          const int cg = c + g * cstep;
           if (v.Is_t)
             for (int tt = 0; tt < m; ++tt) {
               const uint4 sraw = ld_v4(at<T>(v, j * m + tt, v.off.part_s) + (size_t)t * h + cg);
@@ -675,7 +687,7 @@ __device__ __forceinline__ void combine_token_body(const DevView& v) {
         }
       }
     }
-    for (; c < c1; c += 32 * V) {
+    for (; c < c1; c += cstep) {
       A acc[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) acc[q] = (A)0;
@@ -709,10 +721,10 @@ __device__ __forceinline__ void combine_token_body(const DevView& v) {
 }
 
 template <int DT>
-__global__ void __launch_bounds__(256) k_combine_token(DevView v) {
+__global__ void __launch_bounds__(256) k_combine_token(DevView v, int S) {
   pdl_wait();  // predecessor's outputs are visible after this
   if (v.sync_wait) grid_wait(v);  // every host's pushes into ZIN have landed
-  combine_token_body<DT>(v);
+  combine_token_body<DT>(v, S);
   if (v.sync_signal) grid_signal_and_wait(v);  // y complete on every TP rank: barrier #4
 }
 
@@ -790,6 +802,15 @@ static int blocks_for(long long warps) {
   return (int)b;
 }
 
+// Warps per row for the warp-per-row kernels (k_pair_reduce,
+// k_combine_token): split a row's columns over up to 8 warps while the rows
+// alone would not fill one 8-warp CTA per SM (decode batches).
+static int col_split(long long rows) {
+  int S = 1;
+  while (S < 8 && rows * S * 2 <= 148LL * 8) S *= 2;
+  return S;
+}
+
 static int check_vec(const DevView& v) {
   int c0, c1;
   col_shard(v.h, v.m, v.tp_rank, &c0, &c1);
@@ -856,11 +877,12 @@ int launch_pair_reduce(const DevView& v, cudaStream_t s, int part, bool coreside
   }
   // f64 (reference association), long pairs, rows too wide to stage
   const int threads = coresident ? 128 : 256;
-  const int g = coresident ? 148 : blocks_for((long long)v.T * v.n);
+  const int S = coresident ? 1 : col_split((long long)v.T * v.n);
+  const int g = coresident ? 148 : blocks_for((long long)v.T * v.n * S);
   switch (v.elt) {
-    case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, threads, 0, s, v, part); break;
-    case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, threads, 0, s, v, part); break;
-    default: pdl_launch(k_pair_reduce<MX_BF16, float>, g, threads, 0, s, v, part);
+    case 8: pdl_launch(k_pair_reduce<MX_F64, double>, g, threads, 0, s, v, part, S); break;
+    case 4: pdl_launch(k_pair_reduce<MX_F32, float>, g, threads, 0, s, v, part, S); break;
+    default: pdl_launch(k_pair_reduce<MX_BF16, float>, g, threads, 0, s, v, part, S);
   }
   MX_LAUNCH_CHECK();
   return MX_OK;
@@ -908,11 +930,12 @@ int launch_combine_token(const DevView& v, cudaStream_t s) {
   int rc = check_vec(v);
   if (rc) return rc;
   if (v.T == 0) return MX_OK;
-  const int g = blocks_for(v.T);
+  const int S = col_split(v.T);
+  const int g = blocks_for((long long)v.T * S);
   switch (v.elt) {
-    case 8: pdl_launch(k_combine_token<MX_F64>, g, 256, 0, s, v); break;
-    case 4: pdl_launch(k_combine_token<MX_F32>, g, 256, 0, s, v); break;
-    default: pdl_launch(k_combine_token<MX_BF16>, g, 256, 0, s, v);
+    case 8: pdl_launch(k_combine_token<MX_F64>, g, 256, 0, s, v, S); break;
+    case 4: pdl_launch(k_combine_token<MX_F32>, g, 256, 0, s, v, S); break;
+    default: pdl_launch(k_combine_token<MX_BF16>, g, 256, 0, s, v, S);
   }
   MX_LAUNCH_CHECK();
   return MX_OK;

@@ -1,0 +1,180 @@
+// Per-SM DRAM -> shared memory streaming rate vs bytes in flight (bulk
+// copies completing on mbarriers), the ceiling a weight-streaming (decode)
+// GEMM producer can reach.  Each CTA streams its own contiguous region in
+// CH-byte chunks through an S-stage ring; one thread issues, the CTA only
+// waits for completion (no consumer work).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/stream_probe tools/stream_probe.cu
+//   /tmp/stream_probe
+#include <cstdio>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void k_stream(const char* src, size_t per_cta, int ch, int stages, unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* buf = sm + 1024;
+  const char* base = src + blockIdx.x * per_cta;
+  const int nch = (int)(per_cta / ch);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned acc = 0;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(ch) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf + (size_t)s * ch)),
+        "l"(base + (size_t)i * ch), "r"(ch), "r"(smem_u32(&bar[s]))
+        : "memory");
+  };
+  for (int i = 0; i < stages && i < nch; ++i) issue(i);
+  for (int i = 0; i < nch; ++i) {
+    const int s = i % stages;
+    const uint32_t ph = (i / stages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(smem_u32(&bar[s])), "r"(ph) : "memory");
+    acc += buf[(size_t)s * ch];
+    if (i + stages < nch) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
+// Same ring with 2D tensor-map boxes (box_rows x 64 bf16, 128B swizzle):
+// CTA c streams row panel c (box_rows rows) along K, or with tiled = 1 the
+// map views the bytes as [rows*K/64][64] and the box walks contiguous 16 KB.
+__global__ void k_stream2d(const __grid_constant__ CUtensorMap map, int kblocks, int box_rows,
+                           int stages, int tiled, int boxes_per_stage, unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* buf = sm + 1024;
+  const int bytes = box_rows * 128 * boxes_per_stage;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned acc = 0;
+  const int nst = kblocks / boxes_per_stage;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(bytes) : "memory");
+    for (int q = 0; q < boxes_per_stage; ++q) {
+      const int kb = i * boxes_per_stage + q;
+      int c0, c1;
+      if (tiled) { c0 = 0; c1 = (blockIdx.x * kblocks + kb) * box_rows; }
+      else { c0 = kb * 64; c1 = blockIdx.x * box_rows; }
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(buf + (size_t)s * bytes + q * box_rows * 128)),
+          "l"(reinterpret_cast<uint64_t>(&map)), "r"(smem_u32(&bar[s])), "r"(c0), "r"(c1)
+          : "memory");
+    }
+  };
+  for (int i = 0; i < stages && i < nst; ++i) issue(i);
+  for (int i = 0; i < nst; ++i) {
+    const int s = i % stages;
+    const uint32_t ph = (i / stages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(smem_u32(&bar[s])), "r"(ph) : "memory");
+    acc += buf[(size_t)s * bytes];
+    if (i + stages < nst) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
+static void run2d(char* src, unsigned long long* sink, int g, int box_rows, int K, int stages,
+                  int tiled, int bps) {
+  CUtensorMap map;
+  const long long rows = (long long)g * box_rows;
+  cuuint64_t dims[2], strides[1];
+  if (tiled) { dims[0] = 64; dims[1] = rows * (K / 64); strides[0] = 128; }
+  else { dims[0] = K; dims[1] = rows; strides[0] = (cuuint64_t)K * 2; }
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows}, estr[2] = {1, 1};
+  CUresult r = cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box,
+                                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return; }
+  const int kblocks = K / 64;
+  const size_t smem = 1024 + (size_t)stages * box_rows * 128 * bps;
+  cudaFuncSetAttribute(k_stream2d, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  for (int w = 0; w < 2; ++w) k_stream2d<<<g, 32, smem>>>(map, kblocks, box_rows, stages, tiled, bps, sink);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  const int it = 5;
+  for (int i = 0; i < it; ++i) k_stream2d<<<g, 32, smem>>>(map, kblocks, box_rows, stages, tiled, bps, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double sec = ms / 1e3 / it, per = (double)box_rows * K * 2;
+  printf("2D grid %3d box %3dx64 K %6d %s stages %2d x %d boxes (%6d B in flight): %7.1f GB/s total, %6.1f per CTA\n",
+         g, box_rows, K, tiled ? "tiled " : "rowmaj", stages, bps, stages * box_rows * 128 * bps,
+         per * g / sec / 1e9, per / sec / 1e9);
+}
+
+int main() {
+  const size_t total = 1ull << 30;  // 1 GiB source, larger than L2
+  char* src;
+  unsigned long long* sink;
+  cudaMalloc(&src, total);
+  cudaMalloc(&sink, 8);
+  cudaMemset(src, 1, total);
+  cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grids[] = {96, 148};
+  const int chs[] = {4096, 16384, 32768};
+  const int inflight[] = {32768, 65536, 131072, 196608};
+  for (int g : grids)
+    for (int ch : chs)
+      for (int inf : inflight) {
+        const int stages = inf / ch;
+        if (stages < 1 || stages > 64) continue;
+        const size_t per_cta = (size_t)4 << 20;  // 4 MiB per CTA
+        if (per_cta * g > total) continue;
+        const size_t smem = 1024 + (size_t)stages * ch;
+        for (int w = 0; w < 2; ++w) k_stream<<<g, 32, smem>>>(src, per_cta, ch, stages, sink);
+        cudaEventRecord(a);
+        const int it = 5;
+        for (int r = 0; r < it; ++r) k_stream<<<g, 32, smem>>>(src + 0, per_cta, ch, stages, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        const double sec = ms / 1e3 / it;
+        printf("grid %3d  chunk %6d  stages %2d  in-flight %6d B: %7.1f GB/s total, %6.1f GB/s per CTA\n", g,
+               ch, stages, stages * ch, per_cta * g / sec / 1e9, per_cta / sec / 1e9);
+      }
+  for (int g : grids)
+    for (int tiled = 0; tiled < 2; ++tiled) {
+      run2d(src, sink, g, 128, 16384, 6, tiled, 1);   // the GEMM's B ring (BN=128)
+      run2d(src, sink, g, 128, 16384, 12, tiled, 1);
+      run2d(src, sink, g, 256, 8192, 6, tiled, 1);    // BN=256 boxes
+      run2d(src, sink, g, 128, 16384, 3, tiled, 4);   // 4 boxes per stage (64 KB stages)
+    }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+  return 0;
+}
