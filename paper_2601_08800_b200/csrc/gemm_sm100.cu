@@ -220,7 +220,12 @@ struct Args {
   // lifetime -- the effective SM clock the GEMM ran at (power capping
   // lowers it under sustained tensor load; bench.py reports it)
   unsigned long long* clk;
+  // debug timeline (MX_GEMM_TRACE=1): SM clock per CTA at entry [0], setup
+  // done [1], last MMA issued [3], epilogue drained [4], exit [5]
+  unsigned long long* trace;
 };
+#define GEMM_TRACE(i, cond) \
+  do { if (args.trace && (cond)) args.trace[blockIdx.x * 8 + (i)] = clock64(); } while (0)
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -262,8 +267,15 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   __shared__ int s_tstart[MX_EMAX + 1];
   __shared__ int s_off[MX_EMAX];
   __shared__ int s_cnt[MX_EMAX];
+  __shared__ __align__(8) uint64_t s_done;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  GEMM_TRACE(0, threadIdx.x == 0);
+  if (threadIdx.x == 0) {  // descriptors do not depend on earlier kernels
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    if (!args.out_f32) tma_prefetch(&map_d);
+  }
   constexpr int KE = FP8 ? 128 : 64;  // elements per k-block (128 B)
   const int G = args.G, nN = args.N / BN, kblocks = args.K / KE;
 
@@ -292,11 +304,6 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
     }
     if (lane == 0) s_tstart[G] = carry;
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&map_a);
-    tma_prefetch(&map_b);
-    if (!args.out_f32) tma_prefetch(&map_d);
-  }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       // GATHER: the B TMA arrive + one arrive per gathering thread
@@ -307,6 +314,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);  // one arrive per epilogue warp
     }
+    mbar_init(&s_done, 8);  // epilogue warps: every TMEM read and store drained
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -322,6 +330,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   const int total_tiles = s_tstart[G];
   const bool probe = args.clk && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long clk0 = probe ? clock64() : 0, gt0 = probe ? globaltimer_ns() : 0;
+  GEMM_TRACE(1, threadIdx.x == 0);
 
   if (warp == 0 || (GATHER && warp == 3)) {
     if constexpr (GATHER) {
@@ -430,6 +439,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      GEMM_TRACE(3, true);
     }
   } else if (warp >= 4) {
     // ===== epilogue: thread = accumulator row (TMEM lane); two warps per lane
@@ -539,10 +549,23 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       tma_store_wait_all();
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
+    GEMM_TRACE(4, warp == 4 && lane == 0);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_done);
   }
 
+  // End of work: the role branches run single lanes (producer, MMA issuer,
+  // store waits), and the CTA barrier alone was measured not to hold the
+  // non-epilogue warps until the epilogue finished (tools/decode_gemm_bench.py
+  // --trace: thread 0 left it before the last MMA was issued).  Warps 0-3
+  // wait on the epilogue's mbarrier, so the TMEM dealloc, the clock probe and
+  // the fused-barrier signal all follow the last TMEM read and bulk store.
+  if (warp < 4) mbar_wait(&s_done, 0);
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
+  GEMM_TRACE(5, threadIdx.x == 0);
   if (probe) {
     args.clk[0] = clock64() - clk0;
     args.clk[1] = globaltimer_ns() - gt0;
@@ -632,6 +655,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
   __shared__ int s_tstart[MX_EMAX + 1];
   __shared__ int s_off[MX_EMAX];
   __shared__ int s_cnt[MX_EMAX];
+  __shared__ __align__(8) uint64_t s_done;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
@@ -676,6 +700,7 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy)
     }
+    mbar_init(&s_done, 4);  // this CTA's epilogue warps, work drained
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -822,8 +847,14 @@ k_grouped_gemm_pair(const __grid_constant__ CUtensorMap map_a,
       tma_store_wait_all();
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_done);
   }
 
+  // as in k_grouped_gemm: the other warps wait for this CTA's epilogue
+  if (warp < 4) mbar_wait(&s_done, 0);
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   cluster_sync();
@@ -924,6 +955,18 @@ static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   return MX_OK;
 }
 
+// MX_GEMM_TRACE=1: per-CTA phase timestamps of the last grouped GEMM
+// (tools/decode_gemm_bench.py --trace reads them with mx_debug_gemm_trace)
+static unsigned long long* g_trace = nullptr;
+static unsigned long long* gemm_trace_buf() {
+  static const bool on = [] { const char* e = getenv("MX_GEMM_TRACE"); return e && e[0] == '1'; }();
+  if (on && !g_trace) {
+    if (cudaMalloc(&g_trace, 1024 * 8 * 8) != cudaSuccess) g_trace = nullptr;
+    else cudaMemset(g_trace, 0, 1024 * 8 * 8);
+  }
+  return on ? g_trace : nullptr;
+}
+
 // 0: never, 1: auto (dense single-group GEMMs, e.g. the shared expert),
 // 2: always.  Measured (tools/gemm_bench.py): the pair kernel wins on dense
 // shapes (1580 vs 1482 TF/s at 16384x4096x4096) but loses on ragged experts
@@ -978,6 +1021,7 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
     a.sv = *sync; a.sync_wait = sync->sync_wait; a.sync_signal = sync->sync_signal;
     a.clk = at<unsigned long long>(*sync, sync->rank, sync->off.stamps) + (swiglu ? 56 : 58);
   }
+  a.trace = gemm_trace_buf();
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
@@ -1133,3 +1177,9 @@ int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int 
 }
 
 }  // namespace mx
+
+extern "C" __attribute__((visibility("default"))) int mx_debug_gemm_trace(unsigned long long* host, int ctas) {
+  if (!mx::gemm::g_trace || ctas < 1 || ctas > 1024) return -1;
+  if (cudaMemcpy(host, mx::gemm::g_trace, (size_t)ctas * 8 * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return cudaMemset(mx::gemm::g_trace, 0, 1024 * 8 * 8) == cudaSuccess ? 0 : -1;  // next launch starts clean
+}

@@ -31,7 +31,12 @@ def main():
     ap.add_argument("--sets", type=int, default=16)
     ap.add_argument("--cap", type=int, default=0, help="A/D rows allocated (default max(rows, 128))")
     ap.add_argument("--iters", type=int, default=64)
+    ap.add_argument("--trace", action="store_true",
+                    help="per-CTA phase timeline of one more launch (MX_GEMM_TRACE)")
     a = ap.parse_args()
+    if a.trace:
+        import os
+        os.environ["MX_GEMM_TRACE"] = "1"
     gen = torch.Generator().manual_seed(0)
     M = a.active * a.rows
     cap = max(M, a.cap or 128)
@@ -72,6 +77,29 @@ def main():
     print(f"G={a.G} active={a.active} rows={a.rows} N={a.N} K={a.K} swiglu={a.swiglu}: "
           f"median {med:7.2f} us (min {us[0]:.2f})  weights {wbytes / 1e6:.1f} MB -> "
           f"{wbytes / med / 1e3:7.1f} GB/s")
+    if a.trace:
+        import ctypes
+        import numpy as np
+        lib = N.load()
+        buf = np.zeros((1024, 8), dtype=np.uint64)
+        lib.mx_debug_gemm_trace(buf.ctypes.data_as(ctypes.c_void_p), 1024)  # reset
+        flush.fill_(7)
+        run(0)
+        torch.cuda.synchronize()
+        lib.mx_debug_gemm_trace(buf.ctypes.data_as(ctypes.c_void_p), 1024)
+        used = buf[:, 0] > 0
+        t = buf[used].astype(np.int64)
+        t0 = t[:, 0].min()
+        work = t[:, 4] > 0
+        names = ["entry", "setup", "-", "mma_issued", "epilogue_done", "exit"]
+        rel = (t[:, :6] - t[:, :1]) / 1.9e3  # SM cycles -> ~us, per CTA from its entry
+        print(f"  trace: {int(used.sum())} CTAs, {int(work.sum())} with tiles; us from first entry "
+              "(median / max over CTAs with tiles):")
+        for i, nme in enumerate(names):
+            if nme == "-":
+                continue
+            col = rel[work, i]
+            print(f"    {nme:14s} {np.median(col):7.2f} {col.max():7.2f}")
 
 
 if __name__ == "__main__":
