@@ -140,7 +140,16 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// SiLU with the approximate divide (<= 2 ulp; g very negative: the
+// denominator overflows and the quotient is 0, the function's limit).  The
+// IEEE-rounded '/' cost the epilogue ~6 us per 32-column chunk on the
+// decode tiles and made the prefill GEMM1 epilogue-bound in part: 381 ->
+// 367 us at config B (tools/runs/silu_ab.sh; MX_SILU_IEEE keeps it for A/B).
+#ifdef MX_SILU_IEEE
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+#else
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
+#endif
 
 // FP8 dequantisation of 32 accumulator columns: v *= row_scale * col_scale[j]
 __device__ __forceinline__ void scale_cols(uint32_t (&r)[32], float sa, const float* __restrict__ sb) {
@@ -472,8 +481,13 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      GEMM_TRACE(2, warp == 4 && lane == 0);
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if constexpr (SWIGLU) {
+      // a warp whose 32 rows all lie past the group's rows (short tiles:
+      // decode, expert tails) has nothing to store: skip its TMEM reads and math
+      const bool warp_idle = mb * BM + q * 32 >= cnt;
+      if (warp_idle) {
+      } else if constexpr (SWIGLU) {
         // gate/up accumulator columns interleaved in blocks of 64 (w13 packing)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.D) + row * args.ldd + nb * (BN / 2);
 #pragma unroll 1
@@ -540,6 +554,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           }
         }
       }
+      GEMM_TRACE(6, warp == 4 && lane == 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
