@@ -290,6 +290,7 @@ struct mx_plan {
   // fork/join events (created on first use, capturable into a CUDA graph)
   cudaStream_t side = nullptr;
   cudaEvent_t ev[4] = {};
+  bool pf_forked = false;  // decode weight prefetch branch open on `side`
 };
 
 static DevView view_for(const mx_plan* p, int r) {
@@ -819,6 +820,40 @@ static bool overlap_forward(const mx_plan* p) {
          p->d.tokens > 0 && !fused_barriers(p);
 }
 
+// Decode regime: prefetch the active local experts' weights into L2 on the
+// side stream while the dispatch, its barrier and the expand run (see
+// k_prefetch_experts).  Applies when the grouped GEMMs stream weights (at
+// most 64 rows per local expert on average, the GEMM's own decode criterion),
+// SPMD only (one rank per process and device).  MX_PREFETCH_MB: byte budget
+// (default 64 MB, 0 disables).
+static int prefetch_weights(mx_plan* p, const mx_expert_params* ep, cudaStream_t s) {
+  p->pf_forked = false;
+  static const long long budget = [] {
+    const char* e = getenv("MX_PREFETCH_MB");
+    return (e ? atoll(e) : 64LL) << 20;
+  }();
+  mx_comm* c = p->comm;
+  if (budget <= 0 || c->emulate || !ep) return MX_OK;
+  const bool swiglu = p->d.expert_kind == MX_EXPERT_SWIGLU || p->d.expert_kind == MX_EXPERT_SWIGLU_FP8;
+  if (!swiglu || !ep->w13 || !ep->w2) return MX_OK;
+  DevView v = view_for(p, c->rank);
+  const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
+  if (El < 1 || v.cap > 64LL * El) return MX_OK;
+  if (!p->side) {
+    MX_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : p->ev) MX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const size_t wb = p->d.expert_kind == MX_EXPERT_SWIGLU_FP8 ? 1 : 2;
+  const size_t b13 = (size_t)2 * v.I_t * v.h * wb, b2 = (size_t)v.h * v.I_t * wb;
+  MX_CUDA(cudaEventRecord(p->ev[2], s));
+  MX_CUDA(cudaStreamWaitEvent(p->side, p->ev[2], 0));
+  int rc = launch_prefetch_experts(v, ep->w13, ep->w2, b13, b2, budget, p->side);
+  if (rc) return rc;
+  MX_CUDA(cudaEventRecord(p->ev[3], p->side));
+  p->pf_forked = true;
+  return MX_OK;
+}
+
 static int forward_overlapped(mx_plan* p, int rank, const void* x, const float* logits,
                               const int32_t* ids, const void* weights, const mx_expert_params* ep,
                               cudaStream_t s) {
@@ -912,6 +947,8 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
     SyncFlags f(p, fuse, 1, 0);
     if ((rc = mx_layout(p, rank, 0, stream))) return rc;
   }
+  const bool pf = (rc = prefetch_weights(p, ep, s)) == MX_OK && p->pf_forked;
+  if (rc) return rc;
   {
     SyncFlags f(p, fuse, 0, 1);
     if ((rc = mx_dispatch(p, rank, x, stream))) return rc;
@@ -931,6 +968,10 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
       if ((rc = mx_expert_stage(p, rank, ep, st, stream))) return rc;
     if ((rc = launch_reduce_combine(view_for(p, p->comm->rank), s))) return rc;
     if (p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;  // y complete (TP group)
+    if (pf) {
+      MX_CUDA(cudaStreamWaitEvent(s, p->ev[3], 0));
+      p->pf_forked = false;
+    }
     if (y_out) {
       const size_t bytes = (size_t)p->d.tokens * p->d.hidden * elt_bytes(p->d.act_dtype);
       MX_CUDA(cudaMemcpyAsync(y_out, p->comm->heap[p->comm->rank] + p->off.y, bytes,
@@ -954,6 +995,10 @@ int mx_forward(mx_plan* p, int rank, const void* x, const float* logits, const i
   // full barrier (its route only writes count rows read after that barrier);
   // without TP peers (m == 1) y is written by this rank alone: no barrier
   if (!fuse && p->d.tp > 1 && (rc = barrier(p, s, true))) return rc;
+  if (pf) {  // join the prefetch branch (long finished: it only issues hints)
+    MX_CUDA(cudaStreamWaitEvent(s, p->ev[3], 0));
+    p->pf_forked = false;
+  }
   if (y_out) {
     RankIter it;
     if ((rc = ranks_for(p, rank, &it))) return rc;

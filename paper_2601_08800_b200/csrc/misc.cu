@@ -206,3 +206,68 @@ int launch_nvlink_probe(const DevView& v, size_t bytes, cudaStream_t s) {
 }
 
 }  // namespace mx
+
+namespace mx {
+
+// ------------------------------------------------------- expert weight prefetch
+// Decode regime (weight-streaming GEMMs): once the layout has published the
+// per-expert row counts, the weights of this rank's active experts are
+// prefetched into L2 (cp.async.bulk.prefetch) on a side stream while the
+// dispatch, its barrier and the expand run -- the GEMMs then find the first
+// part of their weights in L2 instead of streaming all of it from HBM after
+// the communication.  GEMM1's w13 first, then w2, up to `budget` bytes.
+// Chunks are dealt round-robin over every thread of the grid (the bulk
+// prefetches of one SM alone would serialise in its TMA unit).
+__global__ void __launch_bounds__(128) k_prefetch_experts(DevView v, const char* w13,
+                                                          const char* w2, size_t b13, size_t b2,
+                                                          long long budget) {
+  __shared__ int s_act[MX_EMAX];
+  __shared__ int s_na;
+  const int e0 = first_expert(v.group, v.n, v.E), e1 = first_expert(v.group + 1, v.n, v.E);
+  const int* cnt = at<int>(v, v.rank, v.off.exp_cnt);
+  if (threadIdx.x == 0) {
+    int na = 0;
+    for (int e = e0; e < e1; ++e)
+      if (cnt[e] > 0) s_act[na++] = e - e0;
+    s_na = na;
+  }
+  __syncthreads();
+  const long long na = s_na;
+  const long long t13 = na * (long long)b13, total0 = t13 + na * (long long)b2;
+  const long long total = total0 < budget ? total0 : budget;
+  constexpr long long CH = 32 * 1024;
+  const long long nch = (total + CH - 1) / CH;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nch;
+       c += (long long)gridDim.x * blockDim.x) {
+    long long o = c * CH;
+    const char* base;
+    long long left;
+    if (o < t13) {
+      const long long a = o / (long long)b13, in = o - a * (long long)b13;
+      base = w13 + (size_t)s_act[a] * b13 + in;
+      left = (long long)b13 - in;
+    } else {
+      o -= t13;
+      const long long a = o / (long long)b2, in = o - a * (long long)b2;
+      base = w2 + (size_t)s_act[a] * b2 + in;
+      left = (long long)b2 - in;
+    }
+    long long sz = CH < left ? CH : left;
+    if (sz > total - c * CH) sz = total - c * CH;
+    sz &= ~15LL;
+    if (sz > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base), "r"((unsigned)sz)
+                   : "memory");
+  }
+}
+
+int launch_prefetch_experts(const DevView& v, const void* w13, const void* w2, size_t b13,
+                            size_t b2, long long budget, cudaStream_t s) {
+  if (!w13 || !w2 || budget <= 0) return MX_OK;
+  k_prefetch_experts<<<148, 128, 0, s>>>(v, static_cast<const char*>(w13),
+                                         static_cast<const char*>(w2), b13, b2, budget);
+  MX_LAUNCH_CHECK();
+  return MX_OK;
+}
+
+}  // namespace mx

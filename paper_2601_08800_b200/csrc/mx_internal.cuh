@@ -347,5 +347,7 @@ int quant_rows_e4m3(const void* src, long long lds, void* dst, long long ldd, lo
 int launch_rowsrc_slot(const DevView& v, cudaStream_t s);
 int launch_rowsrc_token(const DevView& v, cudaStream_t s);
 int launch_nvlink_probe(const DevView& v, size_t bytes, cudaStream_t s);
+int launch_prefetch_experts(const DevView& v, const void* w13, const void* w2, size_t b13,
+                            size_t b2, long long budget, cudaStream_t s);
 
 }  // namespace mx
