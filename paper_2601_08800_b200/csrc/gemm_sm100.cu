@@ -230,11 +230,27 @@ struct Args {
   // lowers it under sustained tensor load; bench.py reports it)
   unsigned long long* clk;
   // debug timeline (MX_GEMM_TRACE=1): SM clock per CTA at entry [0], setup
-  // done [1], last MMA issued [3], epilogue drained [4], exit [5]
+  // done [1], last MMA issued [3], epilogue drained [4], exit [5]; wait
+  // cycles [2] [6] [7] in MX_GEMM_WAITSTATS builds
   unsigned long long* trace;
 };
+// MX_GEMM_WAITSTATS (compile-time, variant builds only): cycles the
+// producer spends waiting for free stages [6], the MMA issuer for a free
+// accumulator [7] and for landed stages [2], summed per CTA into the trace
+#ifdef MX_GEMM_WAITSTATS
+#define WAITSTAT(i, stmt)                                                   \
+  do {                                                                      \
+    const long long w0_ = clock64();                                        \
+    stmt;                                                                   \
+    if (args.trace) args.trace[blockIdx.x * 16 + (i)] += clock64() - w0_;    \
+  } while (0)
+#else
+#define WAITSTAT(i, stmt) stmt
+#endif
 #define GEMM_TRACE(i, cond) \
-  do { if (args.trace && (cond)) args.trace[blockIdx.x * 8 + (i)] = clock64(); } while (0)
+  do { if (args.trace && (cond)) args.trace[blockIdx.x * 16 + (i)] = clock64(); } while (0)
+#define GEMM_TRACE_NS(i, cond) \
+  do { if (args.trace && (cond)) args.trace[blockIdx.x * 16 + (i)] = globaltimer_ns(); } while (0)
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -280,6 +296,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   GEMM_TRACE(0, threadIdx.x == 0);
+  GEMM_TRACE_NS(8, threadIdx.x == 0);
   if (threadIdx.x == 0) {  // descriptors do not depend on earlier kernels
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -411,7 +428,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         const int bg = args.b_index ? args.b_index[g] : g;
         const int b_row = bg * args.N + nb * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          WAITSTAT(6, mbar_wait(&empty[stage], phase ^ 1));
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * KE, a_row);
           tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
@@ -428,11 +445,11 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        WAITSTAT(7, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+          WAITSTAT(2, mbar_wait(&full[stage], phase));
           tc_fence_after();
           const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * C::B_BYTES));
@@ -481,7 +498,6 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      GEMM_TRACE(2, warp == 4 && lane == 0);
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
       // a warp whose 32 rows all lie past the group's rows (short tiles:
       // decode, expert tails) has nothing to store: skip its TMEM reads and math
@@ -554,7 +570,6 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
           }
         }
       }
-      GEMM_TRACE(6, warp == 4 && lane == 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -581,6 +596,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   tc_fence_before();
   __syncthreads();
   GEMM_TRACE(5, threadIdx.x == 0);
+  GEMM_TRACE_NS(9, threadIdx.x == 0);
   if (probe) {
     args.clk[0] = clock64() - clk0;
     args.clk[1] = globaltimer_ns() - gt0;
@@ -976,8 +992,8 @@ static unsigned long long* g_trace = nullptr;
 static unsigned long long* gemm_trace_buf() {
   static const bool on = [] { const char* e = getenv("MX_GEMM_TRACE"); return e && e[0] == '1'; }();
   if (on && !g_trace) {
-    if (cudaMalloc(&g_trace, 1024 * 8 * 8) != cudaSuccess) g_trace = nullptr;
-    else cudaMemset(g_trace, 0, 1024 * 8 * 8);
+    if (cudaMalloc(&g_trace, 1024 * 16 * 8) != cudaSuccess) g_trace = nullptr;
+    else cudaMemset(g_trace, 0, 1024 * 16 * 8);
   }
   return on ? g_trace : nullptr;
 }
@@ -1195,6 +1211,6 @@ int launch_expert_swiglu(const DevView& v, const void* w13, const void* w2, int 
 
 extern "C" __attribute__((visibility("default"))) int mx_debug_gemm_trace(unsigned long long* host, int ctas) {
   if (!mx::gemm::g_trace || ctas < 1 || ctas > 1024) return -1;
-  if (cudaMemcpy(host, mx::gemm::g_trace, (size_t)ctas * 8 * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return cudaMemset(mx::gemm::g_trace, 0, 1024 * 8 * 8) == cudaSuccess ? 0 : -1;  // next launch starts clean
+  if (cudaMemcpy(host, mx::gemm::g_trace, (size_t)ctas * 16 * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return cudaMemset(mx::gemm::g_trace, 0, 1024 * 16 * 8) == cudaSuccess ? 0 : -1;  // next launch starts clean
 }

@@ -81,7 +81,7 @@ def main():
         import ctypes
         import numpy as np
         lib = N.load()
-        buf = np.zeros((1024, 8), dtype=np.uint64)
+        buf = np.zeros((1024, 16), dtype=np.uint64)
         lib.mx_debug_gemm_trace(buf.ctypes.data_as(ctypes.c_void_p), 1024)  # reset
         flush.fill_(7)
         run(0)
@@ -91,8 +91,8 @@ def main():
         t = buf[used].astype(np.int64)
         t0 = t[:, 0].min()
         work = t[:, 4] > 0
-        names = ["entry", "setup", "epi_tfull(w4)", "mma_issued", "epilogue_done", "exit", "epi_math(w4)"]
-        rel = (t[:, :7] - t[:, :1]) / 1.9e3  # SM cycles -> ~us, per CTA from its entry
+        names = ["entry", "setup", "-", "mma_issued", "epilogue_done", "exit"]
+        rel = (t[:, :6] - t[:, :1]) / 1.9e3  # SM cycles -> ~us, per CTA from its entry
         print(f"  trace: {int(used.sum())} CTAs, {int(work.sum())} with tiles; us from first entry "
               "(median / max over CTAs with tiles):")
         for i, nme in enumerate(names):

@@ -25,7 +25,13 @@ def main():
     ap.add_argument("--swiglu", action="store_true")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--trace", action="store_true",
+                    help="per-CTA timeline + wait cycles of one more launch (MX_GEMM_TRACE; wait "
+                         "cycles need a -DMX_GEMM_WAITSTATS build via MIXSERVE_B200_LIB)")
     a = ap.parse_args()
+    if a.trace:
+        import os
+        os.environ["MX_GEMM_TRACE"] = "1"
     gen = torch.Generator().manual_seed(0)
     cnts = torch.full((a.G,), a.rows, dtype=torch.int32)
     if a.jitter:
@@ -58,6 +64,29 @@ def main():
                               "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
     except OSError:
         clk = "?"
+    if a.trace:
+        import ctypes
+        import numpy as np
+        lib = N.load()
+        buf = np.zeros((1024, 16), dtype=np.uint64)
+        lib.mx_debug_gemm_trace(buf.ctypes.data_as(ctypes.c_void_p), 1024)  # reset
+        run()
+        torch.cuda.synchronize()
+        lib.mx_debug_gemm_trace(buf.ctypes.data_as(ctypes.c_void_p), 1024)
+        t = buf[buf[:, 0] > 0].astype(np.int64)
+        if len(t) == 0:
+            print("  trace: no CTA recorded (the CTA-pair kernel is not instrumented)")
+            t = None
+    if a.trace and t is not None:
+        mhz = np.median((t[:, 5] - t[:, 0]) / np.maximum(t[:, 9] - t[:, 8], 1) * 1e3)
+        span = (t[:, 9] - t[:, 8]) / 1e3
+        f = lambda col: f"{np.median(col):8.1f} {col.max():8.1f}"
+        print(f"  trace ({len(t)} CTAs, SM clock {mhz:.0f} MHz; us, median / max): CTA span {f(span)}")
+        t = t.astype(np.float64)
+        t[:, [2, 6, 7]] *= 1.9e3 / mhz  # wait cycles -> us below via the /1.9e3
+        print(f"    mma issuer waiting for stages   {f(t[:, 2] / 1.9e3)}")
+        print(f"    mma issuer waiting for TMEM buf {f(t[:, 7] / 1.9e3)}")
+        print(f"    producer waiting for free stage {f(t[:, 6] / 1.9e3)}")
     tf = 2.0 * M * a.N * a.K / (us * 1e-6) / 1e12
     print(f"G={a.G} rows={a.rows}+-{a.jitter} N={a.N} K={a.K} swiglu={a.swiglu}: {us:8.1f} us  {tf:7.1f} TFLOP/s  [{clk}]")
 
