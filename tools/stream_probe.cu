@@ -53,6 +53,48 @@ __global__ void k_stream(const char* src, size_t per_cta, int ch, int stages, un
   if (acc == 0xdeadbeef) *sink = acc;
 }
 
+// L2-resident variant: CTA c streams per_cta bytes starting at
+// (c * 1 MiB) mod (region - per_cta) of a region small enough to stay in L2
+// (warmed by the previous launch), so the copies hit L2.
+__global__ void k_stream_l2(const char* src, size_t per_cta, size_t region, int ch, int stages,
+                            unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* buf = sm + 1024;
+  const char* base = src + ((size_t)blockIdx.x << 20) % (region - per_cta);
+  const int nch = (int)(per_cta / ch);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned acc = 0;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(ch) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf + (size_t)s * ch)),
+        "l"(base + (size_t)i * ch), "r"(ch), "r"(smem_u32(&bar[s]))
+        : "memory");
+  };
+  for (int i = 0; i < stages && i < nch; ++i) issue(i);
+  for (int i = 0; i < nch; ++i) {
+    const int s = i % stages;
+    const uint32_t ph = (i / stages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(smem_u32(&bar[s])), "r"(ph) : "memory");
+    acc += buf[(size_t)s * ch];
+    if (i + stages < nch) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
 // Same ring with 2D tensor-map boxes (box_rows x 64 bf16, 128B swizzle):
 // CTA c streams row panel c (box_rows rows) along K, or with tiled = 1 the
 // map views the bytes as [rows*K/64][64] and the box walks contiguous 16 KB.
@@ -101,6 +143,88 @@ __global__ void k_stream2d(const __grid_constant__ CUtensorMap map, int kblocks,
   if (acc == 0xdeadbeef) *sink = acc;
 }
 
+// L2-resident tensor-map boxes: a [rows][K] bf16 matrix of `region` bytes
+// viewed 3D as (64 cols, rows, K/64 k-blocks) with box (64, box_rows, kb):
+// one instruction brings kb consecutive 128B-swizzled [box_rows][128 B]
+// k-block tiles (the grouped GEMM's operand tiles, kb of them at once).
+// CTA c walks row panel (c % panels) along K, looping over the matrix.
+__global__ void k_stream3d(const __grid_constant__ CUtensorMap map, int kblocks, int box_rows, int kb,
+                           int stages, int panels, int iters, unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* buf = sm + 1024;
+  const int bytes = box_rows * 128 * kb;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned acc = 0;
+  const int per_panel = kblocks / kb;
+  const int nst = per_panel * iters;
+  const int row0 = (blockIdx.x % panels) * box_rows;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    const int k0 = (i % per_panel) * kb;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(buf + (size_t)s * bytes)),
+        "l"(reinterpret_cast<uint64_t>(&map)), "r"(smem_u32(&bar[s])), "r"(0), "r"(row0), "r"(k0)
+        : "memory");
+  };
+  for (int i = 0; i < stages && i < nst; ++i) issue(i);
+  for (int i = 0; i < nst; ++i) {
+    const int s = i % stages;
+    const uint32_t ph = (i / stages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(smem_u32(&bar[s])), "r"(ph) : "memory");
+    acc += buf[(size_t)s * bytes];
+    if (i + stages < nst) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
+static void run3d(char* src, unsigned long long* sink, int g, int box_rows, int kb, int inflight) {
+  const int K = 2048, kblocks = K / 64;
+  const long long rows = (48LL << 20) / (K * 2);  // 48 MiB matrix: L2 resident
+  const int panels = (int)(rows / box_rows);
+  CUtensorMap map;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)kblocks};
+  cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)kb}, estr[3] = {1, 1, 1};
+  CUresult r = cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, src, dims, strides, box,
+                                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { printf("encode3d failed %d\n", (int)r); return; }
+  const int bytes = box_rows * 128 * kb, stages = inflight / bytes;
+  if (stages < 1) return;
+  const int iters = 16;
+  const size_t smem = 1024 + (size_t)stages * bytes;
+  cudaFuncSetAttribute(k_stream3d, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  for (int w = 0; w < 2; ++w) k_stream3d<<<g, 32, smem>>>(map, kblocks, box_rows, kb, stages, panels, iters, sink);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  const int it = 5;
+  for (int i = 0; i < it; ++i) k_stream3d<<<g, 32, smem>>>(map, kblocks, box_rows, kb, stages, panels, iters, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double sec = ms / 1e3 / it, per = (double)box_rows * K * 2 * iters;
+  printf("L2 3D grid %3d box 64x%3dx%d (%6d B/instr, %d stages): %7.1f GB/s total, %6.1f per CTA\n", g, box_rows,
+         kb, bytes, stages, per * g / sec / 1e9, per / sec / 1e9);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+}
+
 static void run2d(char* src, unsigned long long* sink, int g, int box_rows, int K, int stages,
                   int tiled, int bps) {
   CUtensorMap map;
@@ -141,6 +265,7 @@ int main() {
   cudaMalloc(&sink, 8);
   cudaMemset(src, 1, total);
   cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k_stream_l2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -167,6 +292,33 @@ int main() {
         printf("grid %3d  chunk %6d  stages %2d  in-flight %6d B: %7.1f GB/s total, %6.1f GB/s per CTA\n", g,
                ch, stages, stages * ch, per_cta * g / sec / 1e9, per_cta / sec / 1e9);
       }
+  // L2 -> SMEM: every CTA streams a 4 MiB window of a 48 MiB region that
+  // stays resident in L2 (CTA c starts at (c MiB) mod 44 MiB)
+  {
+    const size_t region = (size_t)48 << 20;
+    for (int g : grids)
+      for (int ch : {16384, 32768})
+        for (int inf : {65536, 131072, 196608}) {
+          const int stages = inf / ch;
+          const size_t per_cta = (size_t)4 << 20;
+          const size_t smem = 1024 + (size_t)stages * ch;
+          for (int w = 0; w < 3; ++w) k_stream_l2<<<g, 32, smem>>>(src, per_cta, region, ch, stages, sink);
+          cudaEventRecord(a);
+          const int it = 5;
+          for (int r = 0; r < it; ++r) k_stream_l2<<<g, 32, smem>>>(src, per_cta, region, ch, stages, sink);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          const double sec = ms / 1e3 / it;
+          printf("L2 grid %3d  chunk %6d  stages %2d  in-flight %6d B: %7.1f GB/s total, %6.1f GB/s per CTA\n", g,
+                 ch, stages, stages * ch, per_cta * g / sec / 1e9, per_cta / sec / 1e9);
+        }
+  }
+  for (int g : grids)
+    for (int br : {128, 256})
+      for (int kb : {1, 2, 4})
+        run3d(src, sink, g, br, kb, 196608);
   for (int g : grids)
     for (int tiled = 0; tiled < 2; ++tiled) {
       run2d(src, sink, g, 128, 16384, 6, tiled, 1);   // the GEMM's B ring (BN=128)
