@@ -190,6 +190,81 @@ __global__ void k_stream3d(const __grid_constant__ CUtensorMap map, int kblocks,
   if (acc == 0xdeadbeef) *sink = acc;
 }
 
+// Same L2 stream with `np` issuing threads (lane 0 of warps 0..np-1), warp w
+// owning the ring stages s = w (mod np): is the per-copy cost on the
+// issuing thread (then more issuers help) or in the SM's TMA unit?
+__global__ void k_stream3d_mp(const __grid_constant__ CUtensorMap map, int kblocks, int box_rows,
+                              int stages, int panels, int iters, int np, unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* buf = sm + 1024;
+  const int bytes = box_rows * 128;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) != 0 || w >= np) return;
+  unsigned acc = 0;
+  const int nst = kblocks * iters;
+  const int row0 = (blockIdx.x % panels) * box_rows;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(buf + (size_t)s * bytes)),
+        "l"(reinterpret_cast<uint64_t>(&map)), "r"(smem_u32(&bar[s])), "r"(0), "r"(row0), "r"(i % kblocks)
+        : "memory");
+  };
+  for (int i = w; i < stages && i < nst; i += np) issue(i);
+  for (int i = w; i < nst; i += np) {
+    const int s = i % stages;
+    const uint32_t ph = (i / stages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(smem_u32(&bar[s])), "r"(ph) : "memory");
+    acc += buf[(size_t)s * bytes];
+    if (i + stages < nst) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
+static void run3d_mp(char* src, unsigned long long* sink, int g, int box_rows, int np) {
+  const int K = 2048, kblocks = K / 64;
+  const long long rows = (48LL << 20) / (K * 2);
+  const int panels = (int)(rows / box_rows);
+  CUtensorMap map;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)kblocks};
+  cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1}, estr[3] = {1, 1, 1};
+  CUresult r = cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, src, dims, strides, box,
+                                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { printf("encode3d failed %d\n", (int)r); return; }
+  const int bytes = box_rows * 128, stages = 196608 / bytes, iters = 16;
+  const size_t smem = 1024 + (size_t)stages * bytes;
+  cudaFuncSetAttribute(k_stream3d_mp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  for (int w = 0; w < 2; ++w) k_stream3d_mp<<<g, 128, smem>>>(map, kblocks, box_rows, stages, panels, iters, np, sink);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  const int it = 5;
+  for (int i = 0; i < it; ++i) k_stream3d_mp<<<g, 128, smem>>>(map, kblocks, box_rows, stages, panels, iters, np, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double sec = ms / 1e3 / it, per = (double)box_rows * K * 2 * iters;
+  printf("L2 MP grid %3d box 64x%3d, %d issuing warps: %7.1f GB/s total, %6.1f per CTA\n", g, box_rows, np,
+         per * g / sec / 1e9, per / sec / 1e9);
+}
+
 static void run3d(char* src, unsigned long long* sink, int g, int box_rows, int kb, int inflight) {
   const int K = 2048, kblocks = K / 64;
   const long long rows = (48LL << 20) / (K * 2);  // 48 MiB matrix: L2 resident
@@ -319,6 +394,9 @@ int main() {
     for (int br : {128, 256})
       for (int kb : {1, 2, 4})
         run3d(src, sink, g, br, kb, 196608);
+  for (int br : {128, 256})
+    for (int np : {1, 2, 4})
+      run3d_mp(src, sink, 148, br, np);
   for (int g : grids)
     for (int tiled = 0; tiled < 2; ++tiled) {
       run2d(src, sink, g, 128, 16384, 6, tiled, 1);   // the GEMM's B ring (BN=128)
