@@ -743,11 +743,16 @@ __device__ __forceinline__ void exchange_barrier(const DevView& v) {
     unsigned long long* go = reinterpret_cast<unsigned long long*>(
         reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 8);
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(epoch_ctr(v)) + 1;
-    __threadfence_system();  // this CTA's pushes ordered before its arrival
     const long long t0 = clock64();
-    if (atomicAdd(cnt, 1) == (int)gridDim.x - 1) {
+    // arrival with acq_rel at GPU scope: this CTA's pushes (after the CTA
+    // barrier above) happen-before the last arriver's system-scope release
+    // to the peers, which is cumulative over them -- one fence on the
+    // critical path instead of a system fence per CTA plus two in the last
+    // (the lean device barrier's reasoning, api.cu k_barrier_lean)
+    int arrived;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(arrived) : "l"(cnt) : "memory");
+    if (arrived == (int)gridDim.x - 1) {
       *cnt = 0;
-      __threadfence_system();
       *epoch_ctr(v) = e;
       for (int r = 0; r < v.W; ++r)
         st_release_sys(reinterpret_cast<unsigned long long*>(v.heap[r] + v.off.flags) + v.rank, e);
@@ -755,7 +760,6 @@ __device__ __forceinline__ void exchange_barrier(const DevView& v) {
       for (int r = 0; r < v.W; ++r)
         while (ld_acquire_sys(mine + r) < e)
           if (clock64() - t0 > 20000000000LL) { atomicOr(reinterpret_cast<int*>(v.heap[v.rank] + v.off.err) + 2, 1); break; }
-      __threadfence_system();
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(go), "l"(e) : "memory");
     } else {
       unsigned long long g = 0;
