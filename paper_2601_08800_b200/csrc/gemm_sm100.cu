@@ -233,6 +233,12 @@ struct Args {
   // done [1], last MMA issued [3], epilogue drained [4], exit [5]; wait
   // cycles [2] [6] [7] in MX_GEMM_WAITSTATS builds
   unsigned long long* trace;
+  // decode regime (weight-streaming tiles): `early` -- the group tables and
+  // the weights were written long before the predecessor kernel, so the
+  // schedule is built and the first stages' B boxes are issued before the
+  // PDL wait, which then only gates the A boxes; `trigger` -- let the next
+  // kernel's CTAs launch (and do the same) on the SMs this grid leaves idle
+  int early, trigger;
 };
 // MX_GEMM_WAITSTATS (compile-time, variant builds only): cycles the
 // producer spends waiting for free stages [6], the MMA issuer for a free
@@ -307,8 +313,11 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
 
   // group offsets/counts -> smem (parallel loads), then the per-group tile
   // prefix by one warp-scan pass (G <= MX_EMAX); no per-tile global reads
-  pdl_wait();  // group offsets/counts and A are written by earlier kernels
-  if (args.sync_wait) grid_wait(args.sv);  // peers' rows have landed
+  const bool early = !GATHER && !FP8 && args.early && !args.sync_wait;
+  if (!early) {
+    pdl_wait();  // group offsets/counts and A are written by earlier kernels
+    if (args.sync_wait) grid_wait(args.sv);  // peers' rows have landed
+  }
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
     s_off[g] = args.offs[g];
     s_cnt[g] = args.cnts[g];
@@ -354,6 +363,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   tc_fence_after();
   const uint32_t tmem = s_tmem;
   const int total_tiles = s_tstart[G];
+  if (args.trigger) pdl_trigger();
   const bool probe = args.clk && blockIdx.x == 0 && threadIdx.x == 0;
   const unsigned long long clk0 = probe ? clock64() : 0, gt0 = probe ? globaltimer_ns() : 0;
   GEMM_TRACE(1, threadIdx.x == 0);
@@ -419,7 +429,24 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         mbar_arrive(&full[(stage + C::STAGES - j) % C::STAGES]);
     } else if (lane == 0) {
       // ===== TMA producer
-      int stage = 0;
+      // early start: the first (fresh, empty) stages get their B boxes
+      // before the PDL wait -- expect_tx without an arrival; the stage's one
+      // arrival comes with its A box after the wait
+      int pre = 0;
+      if (early) {
+        for (int t = blockIdx.x; t < total_tiles && pre < C::STAGES; t += gridDim.x) {
+          int g, mb, nb;
+          decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+          const int bg = args.b_index ? args.b_index[g] : g;
+          for (int kb = 0; kb < kblocks && pre < C::STAGES; ++kb, ++pre) {
+            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                             smem_u32(&full[pre])), "r"((uint32_t)C::B_BYTES) : "memory");
+            tma_load_2d(sB + pre * C::B_BYTES, &map_b, &full[pre], kb * KE, bg * args.N + nb * BN);
+          }
+        }
+        pdl_wait();  // A rows are written by the predecessor
+      }
+      int stage = 0, issued = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int g, mb, nb;
@@ -427,11 +454,16 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
         const int a_row = s_off[g] + mb * BM;
         const int bg = args.b_index ? args.b_index[g] : g;
         const int b_row = bg * args.N + nb * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < kblocks; ++kb, ++issued) {
           WAITSTAT(6, mbar_wait(&empty[stage], phase ^ 1));
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * KE, a_row);
-          tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
+          if (issued < pre) {
+            mbar_expect_tx(&full[stage], C::A_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * KE, a_row);
+          } else {
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &map_a, &full[stage], kb * KE, a_row);
+            tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1053,6 +1085,11 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
     a.clk = at<unsigned long long>(*sync, sync->rank, sync->off.stamps) + (swiglu ? 56 : 58);
   }
   a.trace = gemm_trace_buf();
+  // decode regime: start early (B boxes before the PDL wait), and let GEMM2
+  // start early behind GEMM1 (MX_GEMM_EARLY=0 disables, for A/B runs)
+  static const bool early_on = [] { const char* e = getenv("MX_GEMM_EARLY"); return !(e && e[0] == '0'); }();
+  a.early = early_on && small_m && !gather;
+  a.trigger = a.early && swiglu;
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;

@@ -179,7 +179,10 @@ __global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char
 // warp per pair: each 512 B column chunk of the pair's row is loaded once and
 // stored to every slot row of the pair.
 template <class WT>
-__global__ void __launch_bounds__(256) k_expand(DevView v) {
+__global__ void __launch_bounds__(256) k_expand(DevView v, int trigger) {
+  // decode regime: the grouped GEMM1 behind this kernel may launch at once
+  // and stream its first weight boxes while the rows are expanded
+  if (trigger) pdl_trigger();
   pdl_wait();  // predecessor's outputs are visible after this
   if (v.sync_wait) grid_wait(v);
   const int lane = threadIdx.x & 31;
@@ -842,8 +845,11 @@ int launch_dispatch_token(const DevView& v, const void* x, cudaStream_t s, int p
 int launch_expand(const DevView& v, cudaStream_t s, bool coresident) {
   const int threads = coresident ? 128 : 256;
   const int g = coresident ? 148 : blocks_for((long long)v.T * v.n);
-  if (v.elt == 8) pdl_launch(k_expand<double>, g, threads, 0, s, v);
-  else pdl_launch(k_expand<float>, g, threads, 0, s, v);
+  const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
+  static const bool early_on = [] { const char* e = getenv("MX_GEMM_EARLY"); return !(e && e[0] == '0'); }();
+  const int trigger = early_on && v.elt != 8 && El > 0 && v.cap <= 64LL * El;
+  if (v.elt == 8) pdl_launch(k_expand<double>, g, threads, 0, s, v, trigger);
+  else pdl_launch(k_expand<float>, g, threads, 0, s, v, trigger);
   MX_LAUNCH_CHECK();
   return MX_OK;
 }
