@@ -1088,7 +1088,8 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   // decode regime: start early (B boxes before the PDL wait), and let GEMM2
   // start early behind GEMM1 (MX_GEMM_EARLY=0 disables, for A/B runs)
   static const bool early_on = [] { const char* e = getenv("MX_GEMM_EARLY"); return !(e && e[0] == '0'); }();
-  a.early = early_on && small_m && !gather;
+  static const bool early_all = [] { const char* e = getenv("MX_GEMM_EARLY_ALL"); return e && e[0] == '1'; }();
+  a.early = early_on && (small_m || early_all) && !gather;
   a.trigger = a.early && swiglu;
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
