@@ -71,6 +71,7 @@ __global__ void k_barrier(DevView v, int r0, int nr) {
 // tools/barrier_probe.py at 2 GPUs: 3.2 vs 5.1 us per barrier (graph
 // replay, kernel boundary 0.46 us).  MX_BARRIER=0 selects k_barrier above.
 __global__ void k_barrier_lean(DevView v, int r0, int nr) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   unsigned long long* ctr =
       reinterpret_cast<unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 2);
@@ -293,6 +294,21 @@ struct mx_plan {
   bool pf_forked = false;  // decode weight prefetch branch open on `side`
 };
 
+// Decode regime (the grouped GEMMs stream weights: at most 64 rows per
+// local expert on average): the SPMD phase kernels trigger their dependents
+// at entry, so each next phase's CTAs are already resident, waiting in
+// griddepcontrol.wait, when its predecessor completes (MX_PDL_EARLY=0
+// disables, for A/B runs).
+static bool decode_regime(const mx_plan* p, const DevView& v) {
+  static const bool on = [] {
+    const char* e = getenv("MX_PDL_EARLY");
+    return !(e && e[0] == '0');
+  }();
+  const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
+  return on && !p->comm->emulate && !v.sync_signal && !v.sync_wait && El > 0 &&
+         v.cap <= 64LL * El;
+}
+
 static DevView view_for(const mx_plan* p, int r) {
   DevView v = p->base;
   v.rank = r;
@@ -302,6 +318,7 @@ static DevView view_for(const mx_plan* p, int r) {
   v.a_src_rows = p->a_src_rows[r];
   v.sync_signal = p->sync_signal;
   v.sync_wait = p->sync_wait;
+  v.early = decode_regime(p, v) ? 1 : 0;
   return v;
 }
 
@@ -825,12 +842,14 @@ static bool overlap_forward(const mx_plan* p) {
 // k_prefetch_experts).  Applies when the grouped GEMMs stream weights (at
 // most 64 rows per local expert on average, the GEMM's own decode criterion),
 // SPMD only (one rank per process and device).  MX_PREFETCH_MB: byte budget
-// (default 64 MB, 0 disables).
+// (default 0 = off: together with the early-launched phase kernels the
+// side-stream branch cost ~130 us per decode forward on some boxes,
+// tools/runs/decode_diag.sh; 64 for the measured A/B).
 static int prefetch_weights(mx_plan* p, const mx_expert_params* ep, cudaStream_t s) {
   p->pf_forked = false;
   static const long long budget = [] {
     const char* e = getenv("MX_PREFETCH_MB");
-    return (e ? atoll(e) : 64LL) << 20;
+    return (e ? atoll(e) : 0LL) << 20;
   }();
   mx_comm* c = p->comm;
   if (budget <= 0 || c->emulate || !ep) return MX_OK;

@@ -1090,7 +1090,7 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   static const bool early_on = [] { const char* e = getenv("MX_GEMM_EARLY"); return !(e && e[0] == '0'); }();
   static const bool early_all = [] { const char* e = getenv("MX_GEMM_EARLY_ALL"); return e && e[0] == '1'; }();
   a.early = early_on && (small_m || early_all) && !gather;
-  a.trigger = a.early && swiglu;
+  a.trigger = a.early && (swiglu || (sync && sync->early));
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;

@@ -105,6 +105,7 @@ struct DevView {
   int Is_t;           // shared expert intermediate per TP rank (0: none)
   int sync_signal;    // fused barrier: this kernel's last CTA publishes the epoch
   int sync_wait;      // fused barrier: every CTA waits for all peers' epoch at entry
+  int early;          // decode regime: phase kernels trigger their dependents at entry
   const void* a_src;  // GEMM1 gathers A rows from here (x or XBUF), nullptr: RECV
   long long a_src_rows;
   long long cap;

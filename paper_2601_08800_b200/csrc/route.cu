@@ -34,6 +34,7 @@ __device__ __forceinline__ float warp_max_f32(float v) {
 template <class WT, int EV>
 __global__ void __launch_bounds__(256)
 k_gate(DevView v, const float* __restrict__ logits) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -130,6 +131,7 @@ k_gate(DevView v, const float* __restrict__ logits) {
 template <class WT, int EV>
 __global__ void __launch_bounds__(256)
 k_gate_grouped(DevView v, const float* __restrict__ logits) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const long long tok = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -237,6 +239,7 @@ template <class WT>
 __global__ void __launch_bounds__(512)
 k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__ ids_in,
         const WT* __restrict__ w_in) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = v.T, E = v.E, k = v.k, n = v.n;
@@ -380,6 +383,7 @@ k_route(DevView v, const float* __restrict__ logits, const int32_t* __restrict__
 // coalesced over the expert-major [E][C] layout; publishes the group's
 // per-expert totals into every rank's count matrix (peer stores in SPMD).
 __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -421,6 +425,7 @@ __global__ void __launch_bounds__(256) k_route_scan(DevView v) {
 // then the grid writes every slot's expert-major row and token-major index
 // and every (token, host) pair row.
 __global__ void __launch_bounds__(512) k_layout(DevView v) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   if (v.sync_wait) grid_wait(v);  // every group's counts have landed
   extern __shared__ int sm[];

@@ -51,6 +51,7 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 template <class WT>
 __global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char* __restrict__ x,
                                                            int part) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   // DSPLIT warps per token, each moving its slice of the row's 16 B vectors
@@ -313,6 +314,7 @@ struct PairRange {
 // column, same bits).
 template <int DT, class WT>
 __global__ void __launch_bounds__(256, 2) k_pair_reduce(DevView v, int part, int S) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   using T = typename Elt<DT>::T;
   using A = typename Elt<DT>::Acc;
@@ -725,6 +727,7 @@ __device__ __forceinline__ void combine_token_body(const DevView& v, int S = 1) 
 
 template <int DT>
 __global__ void __launch_bounds__(256) k_combine_token(DevView v, int S) {
+  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
   if (v.sync_wait) grid_wait(v);  // every host's pushes into ZIN have landed
   combine_token_body<DT>(v, S);
