@@ -237,7 +237,12 @@ struct Args {
   // the weights were written long before the predecessor kernel, so the
   // schedule is built and the first stages' B boxes are issued before the
   // PDL wait, which then only gates the A boxes; `trigger` -- let the next
-  // kernel's CTAs launch (and do the same) on the SMs this grid leaves idle
+  // kernel's CTAs launch (and do the same) on the SMs this grid leaves idle.
+  // Invariant: some kernel between the layout (the tables' producer) and the
+  // GEMMs triggers its dependents only at exit (the token dispatch), so the
+  // GEMMs cannot start before the layout completed even when every other
+  // phase kernel triggers at entry (tests/spmd_check.py "decode regime"
+  // caught the cascade: wrong outputs before this rule)
   int early, trigger;
 };
 // MX_GEMM_WAITSTATS (compile-time, variant builds only): cycles the

@@ -51,7 +51,10 @@ __device__ __forceinline__ void copy_row(char* dst, const char* src, size_t nbyt
 template <class WT>
 __global__ void __launch_bounds__(256, 2) k_dispatch_token(DevView v, const char* __restrict__ x,
                                                            int part) {
-  if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
+  // no early trigger here (DevView::early): the grouped GEMMs read the
+  // layout's tables before their PDL wait, which is only safe if some kernel
+  // between the layout and them triggers at exit -- this one (its exit
+  // implies its own wait, i.e. the layout's completion)
   pdl_wait();  // predecessor's outputs are visible after this
   const int lane = threadIdx.x & 31;
   // DSPLIT warps per token, each moving its slice of the row's 16 B vectors

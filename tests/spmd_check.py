@@ -248,6 +248,45 @@ def main():
         del exb
         torch.cuda.empty_cache()
 
+    # ---------------- decode regime at config B's dimensions: the weight-
+    # streaming GEMMs (128-column tiles, early start), the phase kernels'
+    # early PDL triggers and the column-split warp kernels, eager and (one
+    # rank per GPU) graph replay, every token against the CPU oracle
+    Hd, Ed, Kd, Id = 2048, 128, 8, 768
+    if (Id // m) % 128:  # config B has no TP4 layout (I/4 = 192)
+        Id = 1024
+    exd = SwiGLUExperts.random(Ed, Hd, Id, seed=11)
+    w13d, w2d = exd.rank_shard(n, m, rank)
+    oexd = None
+    if rank == 0:
+        oexd = orc.SwiGLUOracle(exd.w_gate.float().cpu().numpy(), exd.w_up.float().cpu().numpy(),
+                                exd.w_down.float().cpu().numpy())
+    for Td in (1, 16):
+        Tgd = Td * n
+        gend = torch.Generator(device="cuda").manual_seed(500 + Td)
+        xd = torch.randn(Tgd, Hd, device="cuda", generator=gend).to(torch.bfloat16)
+        ld = torch.randn(Tgd, Ed, device="cuda", generator=gend)
+        dec = MoELayer(n, m, Td, Hd, Ed, Kd, Id, w13=w13d, w2=w2d, rank=rank, wire="token")
+        xs_d, ls_d = xd[g * Td:(g + 1) * Td].contiguous(), ld[g * Td:(g + 1) * Td].contiguous()
+        yd = fwd(dec, xs_d, ls_d).clone()
+        if not SAME_DEVICE:
+            yd_g = dec.capture(xs_d, ls_d)().clone()
+            torch.cuda.synchronize()
+            if not torch.equal(yd, yd_g):
+                failures.append(f"decode T={Td}: graph replay differs from eager")
+        yds = gather_rows(yd, world)
+        dec.close()
+        if rank == 0:
+            idsd, wd = orc.router_topk(ld.cpu().numpy(), Kd)
+            y_refd = orc.moe_layer_swiglu(xd.float().cpu().numpy(), idsd, wd, oexd)
+            got = torch.cat([yds[j * m] for j in range(n)]).float().cpu().numpy()
+            ed = orc.verify_metric(got, y_refd)
+            print(f"decode regime ({n}x{m}, {Tgd} tokens, config B dims): err {ed:.3e}", flush=True)
+            if ed > 2e-2:
+                failures.append(f"decode T_g={Tgd}: err {ed:.3e}")
+    del exd, w13d, w2d, oexd
+    torch.cuda.empty_cache()
+
     # ---------------- capacity below the routed rows: every rank raises
     from paper_2601_08800_b200 import CapacityError
     T, h, E, k, I = 64, 256, 16, 4, 512
