@@ -1094,7 +1094,11 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   // start early behind GEMM1 (MX_GEMM_EARLY=0 disables, for A/B runs)
   static const bool early_on = [] { const char* e = getenv("MX_GEMM_EARLY"); return !(e && e[0] == '0'); }();
   static const bool early_all = [] { const char* e = getenv("MX_GEMM_EARLY_ALL"); return e && e[0] == '1'; }();
-  a.early = early_on && (small_m || early_all) && !gather;
+  // multi-GPU prefill too: the next GEMM's CTAs fill the SMs of the previous
+  // kernel's last wave (N=4: EP4 0.2922 -> 0.2886 ms, TP2xEP2 0.3165 ->
+  // 0.3117; N=2 -0.25%, N=1 neutral -- profiles/r02_early_all_*)
+  const bool spmd = sync && sync->W > 1;
+  a.early = early_on && (small_m || early_all || spmd) && !gather;
   a.trigger = a.early && (swiglu || (sync && sync->early));
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
   if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }

@@ -854,7 +854,7 @@ int launch_expand(const DevView& v, cudaStream_t s, bool coresident) {
   const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
   static const bool early_on = [] { const char* e = getenv("MX_GEMM_EARLY"); return !(e && e[0] == '0'); }();
   static const bool early_all = [] { const char* e = getenv("MX_GEMM_EARLY_ALL"); return e && e[0] == '1'; }();
-  const int trigger = early_on && v.elt != 8 && El > 0 && (v.cap <= 64LL * El || early_all);
+  const int trigger = early_on && v.elt != 8 && El > 0 && (v.cap <= 64LL * El || early_all || v.W > 1);
   if (v.elt == 8) pdl_launch(k_expand<double>, g, threads, 0, s, v, trigger);
   else pdl_launch(k_expand<float>, g, threads, 0, s, v, trigger);
   MX_LAUNCH_CHECK();
