@@ -304,9 +304,13 @@ static bool decode_regime(const mx_plan* p, const DevView& v) {
     const char* e = getenv("MX_PDL_EARLY");
     return !(e && e[0] == '0');
   }();
+  static const bool all = [] {
+    const char* e = getenv("MX_PDL_EARLY_ALL");
+    return e && e[0] == '1';
+  }();
   const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
   return on && !p->comm->emulate && !v.sync_signal && !v.sync_wait && El > 0 &&
-         v.cap <= 64LL * El;
+         (v.cap <= 64LL * El || (all && v.W > 1));
 }
 
 static DevView view_for(const mx_plan* p, int r) {
