@@ -244,6 +244,9 @@ struct Args {
   // phase kernel triggers at entry (tests/spmd_check.py "decode regime"
   // caught the cascade: wrong outputs before this rule)
   int early, trigger;
+  // GATHER with TMA tile::gather4 (map_a: the source rows, 64 x 1 boxes):
+  // 32 four-row gathers per k-block, issued by three threads in parallel
+  int gather4;
 };
 // MX_GEMM_WAITSTATS (compile-time, variant builds only): cycles the
 // producer spends waiting for free stages [6], the MMA issuer for a free
@@ -347,7 +350,7 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       // GATHER: the B TMA arrive + one arrive per gathering thread
-      mbar_init(&full[s], GATHER ? 1 + GATHER_THREADS : 1);
+      mbar_init(&full[s], GATHER && !args.gather4 ? 1 + GATHER_THREADS : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -373,8 +376,57 @@ k_grouped_gemm(const __grid_constant__ CUtensorMap map_a,
   const unsigned long long clk0 = probe ? clock64() : 0, gt0 = probe ? globaltimer_ns() : 0;
   GEMM_TRACE(1, threadIdx.x == 0);
 
-  if (warp == 0 || (GATHER && warp == 3)) {
-    if constexpr (GATHER) {
+  if (warp == 0 || (GATHER && (warp == 3 || (args.gather4 && warp == 2)))) {
+    if (GATHER && args.gather4) {
+      if (lane == 0) {
+        // ===== gather4 producers (lane 0 of warps 0, 2, 3): each k-block's
+        // A tile = 32 tile::gather4 copies of 4 rows x 128 B (the TMA unit
+        // applies the 128B swizzle by smem address, as for a 128-row box);
+        // warp w issues gathers [q0, q1) -- one issuing thread capped the
+        // feed (round 1: 964 us for GEMM1) -- warp 0 also the B box and the
+        // stage's one arrival (expect_tx of A + B: the other issuers' copies
+        // may complete first, the tx-count then dips below zero meanwhile).
+        const int w = warp == 0 ? 0 : warp == 2 ? 1 : 2;
+        const int q0 = (32 * w) / 3, q1 = (32 * (w + 1)) / 3;  // 0-10, 10-21, 21-32
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+          int g, mb, nb;
+          decode_tile(t, s_tstart, G, nN, &g, &mb, &nb);
+          const int bg = args.b_index ? args.b_index[g] : g;
+          const int b_row = bg * args.N + nb * BN;
+          const int cnt = s_cnt[g];
+          int rows[11][4];
+#pragma unroll
+          for (int q = 0; q < 11; ++q)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r_local = mb * BM + 4 * (q0 + q) + j;
+              rows[q][j] = (q0 + q < q1 && r_local < cnt)
+                               ? args.a_rows[(long long)s_off[g] + r_local] : -1;
+            }
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (w == 0) {
+              mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+              tma_load_2d(sB + stage * C::B_BYTES, &map_b, &full[stage], kb * KE, b_row);
+            }
+            const uint32_t dst = smem_u32(sA + stage * C::A_BYTES);
+#pragma unroll
+            for (int q = 0; q < 11; ++q)
+              if (q0 + q < q1)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::"
+                    "complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(
+                        dst + (q0 + q) * 512),
+                    "l"(reinterpret_cast<uint64_t>(&map_a)), "r"(smem_u32(&full[stage])),
+                    "r"(kb * KE), "r"(rows[q][0]), "r"(rows[q][1]), "r"(rows[q][2]), "r"(rows[q][3])
+                    : "memory");
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    } else if constexpr (GATHER) {
       // ===== gathering producer (warps 0 and 3): A rows come from an
       // arbitrary row table (token rows of x / XBUF), so they are brought
       // with 16 B LDGSTS into the 128B-swizzled layout the UMMA descriptor
@@ -1072,13 +1124,17 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   CUtensorMap ma, mb, md;
   memset(&md, 0, sizeof(md));
   const bool gather = a_rows != nullptr;
-  (void)a_src_rows;
+
   // B rows: every group's N rows (b_index may address any of them)
   long long b_rows = (long long)G * N;
   int rc = make_map(&mb, B, b_rows, K, bn);
   if (rc) return rc;
-  // gathered A is read with LDGSTS through a_rows (no tensor map)
-  if (gather) ma = mb;
+  // gathered A: LDGSTS through a_rows (no tensor map), or (MX_GATHER4=1)
+  // tile::gather4 through a 64 x 1-row box map over the source rows
+  const char* g4_env = getenv("MX_GATHER4");  // read per call (tests toggle it)
+  const bool g4 = g4_env && g4_env[0] == '1';
+  if (gather && g4) { if ((rc = make_map(&ma, A, a_src_rows, K, 1))) return rc; }
+  else if (gather) ma = mb;
   else if ((rc = make_map(&ma, A, M_cap, K, BM))) return rc;
   if (out_dtype == MX_BF16) {  // 32x32 output boxes, 64 B swizzle (staged epilogue)
     rc = make_map(&md, D, M_cap, swiglu ? N / 2 : N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -1101,7 +1157,7 @@ int grouped_gemm(const void* A, const void* B, void* D, int out_dtype, const int
   a.early = early_on && (small_m || early_all || spmd) && !gather;
   a.trigger = a.early && (swiglu || (sync && sync->early));
   a.D = D; a.offs = offs; a.cnts = cnts; a.b_index = b_index; a.a_rows = a_rows;
-  if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; }
+  if (gather) { a.a_base = static_cast<const char*>(A); a.lda = (long long)K * 2; a.gather4 = g4; }
   a.G = G; a.N = N; a.K = K; a.ldd = swiglu ? N / 2 : N; a.out_f32 = out_dtype == MX_F32;
   a.M_cap = M_cap;
   // upper bound on tiles (host does not know the per-group counts)

@@ -473,12 +473,14 @@ def test_gathered_gemm1_equals_copied_rows(wire, monkeypatch):
     x = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
     logits = torch.randn(T, E, device="cuda", generator=gen)
     outs = {}
-    for g in ("0", "1"):
-        monkeypatch.setenv("MX_GATHER", g)
+    for g in ("0", "1", "4"):  # copy, LDGSTS gather, TMA tile::gather4
+        monkeypatch.setenv("MX_GATHER", "0" if g == "0" else "1")
+        monkeypatch.setenv("MX_GATHER4", "1" if g == "4" else "0")
         layer = MoELayer(1, 1, T, h, E, k, I, experts=ex, rank=0, wire=wire)
         outs[g] = layer.forward(x, logits).clone()
         layer.close()
     assert torch.equal(outs["0"], outs["1"])
+    assert torch.equal(outs["0"], outs["4"])
     oex = orc.SwiGLUOracle(ex.w_gate.float().cpu().numpy(), ex.w_up.float().cpu().numpy(),
                            ex.w_down.float().cpu().numpy())
     ids, w = orc.router_topk(logits.cpu().numpy(), k)
