@@ -7,6 +7,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/stream_probe tools/stream_probe.cu
 //   /tmp/stream_probe
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -265,6 +266,73 @@ static void run3d_mp(char* src, unsigned long long* sink, int g, int box_rows, i
          per * g / sec / 1e9, per / sec / 1e9);
 }
 
+// 4 KB bulk copies (the pair pre-reduction's slot rows) from DRAM with
+// `lanes` issuing lanes in each of `nw` warps: lane l of warp w owns ring
+// slots s = w*lanes + l (mod stages) -- are several lanes of one warp
+// several issuers?
+__global__ void k_stream_lanes(const char* src, size_t per_cta, int stages, int lanes, int nw,
+                               unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  unsigned char* buf = sm + 1024;
+  const int ch = 4096;
+  const char* base = src + blockIdx.x * per_cta;
+  const int nch = (int)(per_cta / ch);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (w >= nw || l >= lanes) return;
+  const int me = w * lanes + l, np = nw * lanes;
+  unsigned acc = 0;
+  auto issue = [&](int i) {
+    const int s = i % stages;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(ch) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf + (size_t)s * ch)),
+        "l"(base + (size_t)i * ch), "r"(ch), "r"(smem_u32(&bar[s]))
+        : "memory");
+  };
+  for (int i = me; i < stages && i < nch; i += np) issue(i);
+  for (int i = me; i < nch; i += np) {
+    const int s = i % stages;
+    const uint32_t ph = (i / stages) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(smem_u32(&bar[s])), "r"(ph) : "memory");
+    acc += buf[(size_t)s * ch];
+    if (i + stages < nch) issue(i + stages);
+  }
+  if (acc == 0xdeadbeef) *sink = acc;
+}
+
+static void run_lanes(char* src, unsigned long long* sink, int g, int lanes, int nw) {
+  const int stages = 48;  // 192 KB of 4 KB slots
+  const size_t per_cta = (size_t)4 << 20;
+  const size_t smem = 1024 + (size_t)stages * 4096;
+  cudaFuncSetAttribute(k_stream_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  for (int w = 0; w < 2; ++w) k_stream_lanes<<<g, 256, smem>>>(src, per_cta, stages, lanes, nw, sink);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  const int it = 5;
+  for (int i = 0; i < it; ++i) k_stream_lanes<<<g, 256, smem>>>(src, per_cta, stages, lanes, nw, sink);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double sec = ms / 1e3 / it;
+  printf("4KB bulk grid %3d, %d warps x %d lanes issuing: %7.1f GB/s total, %6.1f per CTA\n", g, nw, lanes,
+         per_cta * g / sec / 1e9, per_cta / sec / 1e9);
+}
+
 static void run3d(char* src, unsigned long long* sink, int g, int box_rows, int kb, int inflight) {
   const int K = 2048, kblocks = K / 64;
   const long long rows = (48LL << 20) / (K * 2);  // 48 MiB matrix: L2 resident
@@ -341,6 +409,12 @@ int main() {
   cudaMemset(src, 1, total);
   cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   cudaFuncSetAttribute(k_stream_l2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (getenv("PROBE_LANES_ONLY")) {  // 4 KB bulk copies vs issuing lanes/warps only
+    for (int nw : {1, 2, 4})
+      for (int lanes : {1, 8, 16})
+        run_lanes(src, sink, 148, lanes, nw);
+    return 0;
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
