@@ -73,11 +73,16 @@ __global__ void k_barrier(DevView v, int r0, int nr) {
 __global__ void k_barrier_lean(DevView v, int r0, int nr) {
   if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
-  unsigned long long* ctr =
-      reinterpret_cast<unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 2);
-  const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(ctr) + 1;
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) {  // one read and one bump of the epoch counter per barrier
+    unsigned long long* ctr =
+        reinterpret_cast<unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 2);
+    s_epoch = *reinterpret_cast<volatile unsigned long long*>(ctr) + 1;
+    *ctr = s_epoch;
+  }
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
   const int r = r0 + threadIdx.x;
-  if (threadIdx.x == 0) *ctr = epoch;
   if ((int)threadIdx.x < nr) {
     st_release_sys(at<unsigned long long>(v, r, v.off.flags) + v.rank, epoch);
     const unsigned long long* mine = at<unsigned long long>(v, v.rank, v.off.flags) + r;
