@@ -73,15 +73,24 @@ __global__ void k_barrier(DevView v, int r0, int nr) {
 __global__ void k_barrier_lean(DevView v, int r0, int nr) {
   if (v.early) pdl_trigger();  // decode: the next phase launches now, waits in griddepcontrol.wait
   pdl_wait();  // predecessor's outputs are visible after this
+  // one read and one bump of the epoch counter per barrier, broadcast by a
+  // shuffle (one warp: worlds up to 32 ranks) or through shared memory
   __shared__ unsigned long long s_epoch;
-  if (threadIdx.x == 0) {  // one read and one bump of the epoch counter per barrier
+  unsigned long long e0 = 0;
+  if (threadIdx.x == 0) {
     unsigned long long* ctr =
         reinterpret_cast<unsigned long long*>(at<int>(v, v.rank, v.off.counters) + 2);
-    s_epoch = *reinterpret_cast<volatile unsigned long long*>(ctr) + 1;
-    *ctr = s_epoch;
+    e0 = *reinterpret_cast<volatile unsigned long long*>(ctr) + 1;
+    *ctr = e0;
+    s_epoch = e0;
   }
-  __syncthreads();
-  const unsigned long long epoch = s_epoch;
+  unsigned long long epoch;
+  if (blockDim.x <= 32) {
+    epoch = __shfl_sync(0xffffffffu, e0, 0);
+  } else {
+    __syncthreads();
+    epoch = s_epoch;
+  }
   const int r = r0 + threadIdx.x;
   if ((int)threadIdx.x < nr) {
     st_release_sys(at<unsigned long long>(v, r, v.off.flags) + v.rank, epoch);
