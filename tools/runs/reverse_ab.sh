@@ -1,0 +1,11 @@
+#!/bin/bash
+for r in 1 2; do
+for v in 0 1; do
+  MX_GEMM_REVERSE=$v timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/rv.json 2> gpurun_out/rv.err
+  python -c "
+import json
+d=json.load(open('gpurun_out/rv.json')); p=d['phases_us']; print('r$r REVERSE=$v', round(d['ms_per_step'],4), 'gemm1', round(p['gemm1_swiglu'],1), 'gemm2', round(p['gemm2'],1), 'combine', round(p['combine'],1))
+" || tail -5 gpurun_out/rv.err
+done
+done
+MX_GEMM_REVERSE=1 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gemm or swiglu" 2>&1 | tail -1
