@@ -323,8 +323,10 @@ static bool decode_regime(const mx_plan* p, const DevView& v) {
     return e && e[0] == '1';
   }();
   const int El = first_expert(v.group + 1, v.n, v.E) - first_expert(v.group, v.n, v.E);
+  // (at 1-2 tokens per group the parked CTAs cost more than the launches
+  // they hide: EP2 T_g = 2 77.0 vs 74.3 us, profiles/r02_decode_diag_n4.log)
   return on && !p->comm->emulate && !v.sync_signal && !v.sync_wait && El > 0 &&
-         (v.cap <= 64LL * El || (all && v.W > 1));
+         ((v.cap <= 64LL * El && v.T >= 4) || (all && v.W > 1));
 }
 
 static DevView view_for(const mx_plan* p, int r) {
