@@ -880,8 +880,13 @@ int launch_pair_reduce(const DevView& v, cudaStream_t s, int part, bool coreside
   // every SM 32 pairs (decode) keep the register kernel's single latency
   // chain per pair.  Its ~200 KB ring cannot share an SM with a GEMM CTA, so
   // co-resident launches and the non-contiguous part 2 use the register kernel.
-  if (!coresident && part != 2 && v.elt != 8 && v.k <= 4 * v.n &&
-      (long long)v.T * v.n >= 148LL * 32 && prb_slots(row_bytes) >= PRB_KU) {
+  // The ring must also hold several pairs' rows: config C's 14 KB rows leave
+  // 14 slots (fewer than two full pairs) and the register kernel is faster
+  // there (TP2xEP2 at 4 GPUs: 192 vs 330 us, layer 1.554 vs 1.681 ms;
+  // profiles/r02_prb_wide_rows_ab.log).  MX_PRB=0 forces the register kernel.
+  static const int prb_env = [] { const char* e = getenv("MX_PRB"); return e ? atoi(e) : -1; }();
+  if (prb_env != 0 && !coresident && part != 2 && v.elt != 8 && v.k <= 4 * v.n &&
+      (long long)v.T * v.n >= 148LL * 32 && prb_slots(row_bytes) >= 3 * PRB_KU) {
     auto kern = v.elt == 4 ? k_pair_reduce_bulk<MX_F32> : k_pair_reduce_bulk<MX_BF16>;
     static bool attr[2] = {false, false};
     if (!attr[v.elt == 4]) {
@@ -912,7 +917,7 @@ int launch_pair_reduce(const DevView& v, cudaStream_t s, int part, bool coreside
 bool reduce_combine_ok(const DevView& v) {
   const size_t row_bytes = (size_t)v.h * v.elt;
   return !(v.elt == 8 || v.k > 4 * v.n || (long long)v.T * v.n < 148LL * 32 ||
-           prb_slots(row_bytes) < PRB_KU || v.T == 0 || v.W < 2);
+           prb_slots(row_bytes) < 3 * PRB_KU || v.T == 0 || v.W < 2);
 }
 
 int launch_reduce_combine(const DevView& v, cudaStream_t s) {
