@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 # two producer warps in the bulk pre-reduction: parity (4 GPUs + fused combine path) and A/B vs HEAD
 R4="python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr=127.0.0.1"
 R2="python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr=127.0.0.1"

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 for r in 1 2; do
 for v in 0 1; do
   MX_GEMM_REVERSE=$v timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/rv.json 2> gpurun_out/rv.err

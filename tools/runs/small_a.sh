@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 # small A boxes for short tiles: A/B on the decode GEMM shapes, then GEMM parity tests
 for t in 0 1; do
   echo "== MX_GEMM_SMALL_A=$t"

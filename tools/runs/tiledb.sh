@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 # experiment: B boxes contiguous in HBM (MX_GEMM_TILEDB=1, numerics garbage) vs row-major weights
 for t in 0 1; do
   echo "== MX_GEMM_TILEDB=$t"

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 # two TMA producer threads (A / B) vs one, grouped GEMM shapes, then tests and the N=1 bench
 for r in 1 2; do
  for L in paper_2601_08800_b200/lib/variants/libmx_head.so paper_2601_08800_b200/lib/libmixserve_b200.so; do
