@@ -1,5 +1,4 @@
 #!/bin/bash
-# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 # A/B: HEAD grouped GEMM (lib/variants/libmx_head.so) vs working tree, interleaved
 for r in 1 2; do
  for L in paper_2601_08800_b200/lib/variants/libmx_head.so paper_2601_08800_b200/lib/libmixserve_b200.so; do

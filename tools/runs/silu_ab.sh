@@ -1,5 +1,4 @@
 #!/bin/bash
-# (experiment: the code it toggles was reverted after this A/B; the numbers are in DESIGN.md §5/§8)
 for L in paper_2601_08800_b200/lib/libmixserve_b200.so paper_2601_08800_b200/lib/variants/libmx_silu_IEEE.so; do
   echo "== $L"
   MIXSERVE_B200_LIB=$L timeout 120 python tools/decode_gemm_bench.py --trace --active 8 --rows 2 --N 1536 --K 2048 --swiglu | grep -E "median|epi_|mma_issued"
