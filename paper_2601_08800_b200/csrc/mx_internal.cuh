@@ -224,13 +224,20 @@ inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 __device__ __forceinline__ unsigned long long* epoch_ctr(const DevView& v) {
   return reinterpret_cast<unsigned long long*>(reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 2);
 }
+// Arrival per CTA with acq_rel at GPU scope (the CTA's writes, local and
+// remote, happen-before the last arriver's system-scope release to the
+// peers, which is cumulative over them): one system fence on the critical
+// path, as in the lean device barrier (api.cu k_barrier_lean).
+__device__ __forceinline__ int arrive_acq_rel_gpu(int* ctr) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+  return old;
+}
 __device__ __forceinline__ void grid_signal(const DevView& v) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
     int* ctr = reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 4;
-    if (atomicAdd(ctr, 1) == (int)(gridDim.x * gridDim.y) - 1) {
-      __threadfence_system();
+    if (arrive_acq_rel_gpu(ctr) == (int)(gridDim.x * gridDim.y) - 1) {
       *ctr = 0;
       const unsigned long long e = ++(*epoch_ctr(v));
       for (int r = 0; r < v.W; ++r)
@@ -259,11 +266,9 @@ __device__ __forceinline__ void grid_signal_and_wait(const DevView& v) {
   __syncthreads();
   __shared__ int s_is_last;
   if (threadIdx.x == 0) {
-    __threadfence_system();
     int* ctr = reinterpret_cast<int*>(v.heap[v.rank] + v.off.counters) + 4;
-    s_is_last = atomicAdd(ctr, 1) == (int)(gridDim.x * gridDim.y) - 1;
+    s_is_last = arrive_acq_rel_gpu(ctr) == (int)(gridDim.x * gridDim.y) - 1;
     if (s_is_last) {
-      __threadfence_system();
       *ctr = 0;
       const unsigned long long e = ++(*epoch_ctr(v));
       for (int r = 0; r < v.W; ++r)
