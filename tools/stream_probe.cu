@@ -248,6 +248,7 @@ static void run3d_mp(char* src, unsigned long long* sink, int g, int box_rows, i
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { printf("encode3d failed %d\n", (int)r); return; }
   const int bytes = box_rows * 128, stages = 196608 / bytes, iters = 16;
+  if (stages % np) return;  // each issuing warp must own whole ring positions
   const size_t smem = 1024 + (size_t)stages * bytes;
   cudaFuncSetAttribute(k_stream3d_mp, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   for (int w = 0; w < 2; ++w) k_stream3d_mp<<<g, 128, smem>>>(map, kblocks, box_rows, stages, panels, iters, np, sink);
@@ -314,6 +315,7 @@ __global__ void k_stream_lanes(const char* src, size_t per_cta, int stages, int 
 
 static void run_lanes(char* src, unsigned long long* sink, int g, int lanes, int nw) {
   const int stages = 48;  // 192 KB of 4 KB slots
+  if (stages % (lanes * nw)) return;  // each issuer must own whole ring positions
   const size_t per_cta = (size_t)4 << 20;
   const size_t smem = 1024 + (size_t)stages * 4096;
   cudaFuncSetAttribute(k_stream_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
