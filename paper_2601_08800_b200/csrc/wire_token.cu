@@ -18,7 +18,10 @@
 
 namespace mx {
 
-constexpr int DSPLIT = 2;  // warps per token in the dispatch
+#ifndef MX_DSPLIT
+#define MX_DSPLIT 2
+#endif
+constexpr int DSPLIT = MX_DSPLIT;  // warps per token in the dispatch
 
 // One pair-list entry: expert-major row of the slot and its top-k weight,
 // written with a single remote store.
