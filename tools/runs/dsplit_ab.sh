@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment: the default stays DSPLIT=2; numbers in DESIGN.md §8)
 # (experiment) four warps per token in the token dispatch (MX_DSPLIT=4 build) vs two, EP4 / TP2xEP2
 R4="python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr=127.0.0.1"
 for r in 1 2; do
