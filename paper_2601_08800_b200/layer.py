@@ -50,6 +50,33 @@ def layout_for(world: int, tp: int | str | None = None, *, routing=None, num_exp
     return world // tp, tp
 
 
+def tp_ep_groups(n: int, m: int, rank: int):
+    """(EP group, TP group) of ``rank`` in the n x m layout, rank ``d*m + t``
+    node-major (sim:63-67): the EP group is the n ranks with the same TP
+    index t (the all-to-all peers of ``_run_baseline``, sim:598-680), the TP
+    group the m ranks of node d (its all-reduce).  Collective: every rank
+    must call it, in the same order, since ``new_group`` is."""
+    if not dist.is_initialized():
+        raise RuntimeError("tp_ep_groups needs an initialised process group")
+    if dist.get_world_size() < n * m:
+        raise ValueError(f"layout {n}x{m} needs {n * m} ranks, world has {dist.get_world_size()}")
+    ep = [dist.new_group([d * m + t for d in range(n)]) for t in range(m)]
+    tp = [dist.new_group([j * m + t for t in range(m)]) for j in range(n)]
+    group, t = divmod(rank, m)
+    return ep[t], tp[group]
+
+
+def baseline_splits(S, group: int):
+    """Row split sizes of node ``group``'s two all-to-alls (sim:617-640):
+    ``send[d]`` = its slots hosted on node d (row ``S[group]``), ``recv[j]``
+    = node j's slots it hosts (column ``S[:, group]``).  The dispatch sends
+    ``send`` and receives ``recv``; the combine swaps them."""
+    S = np.asarray(S)
+    if S.ndim != 2 or S.shape[0] != S.shape[1] or not 0 <= group < S.shape[0]:
+        raise ValueError(f"send matrix {S.shape} has no node {group}")
+    return [int(v) for v in S[group]], [int(v) for v in S[:, group]]
+
+
 class MoELayer:
     def __init__(self, n, m, tokens_per_group, hidden, num_experts, top_k,
                  inter, experts: SwiGLUExperts | None = None, *, rank=None,
@@ -235,12 +262,7 @@ class MoELayer:
     # ------------------------------------------------------------ NCCL baseline
     def _groups(self):
         if self._ep_group is None:
-            n, m = self.n, self.m
-            # every rank must create every group, in the same order
-            ep = [dist.new_group([d * m + t for d in range(n)]) for t in range(m)]
-            tp = [dist.new_group([j * m + t for t in range(m)]) for j in range(n)]
-            self._ep_group = ep[self.tp_rank]
-            self._tp_group = tp[self.group]
+            self._ep_group, self._tp_group = tp_ep_groups(self.n, self.m, self.rank)
         return self._ep_group, self._tp_group
 
     def forward_baseline(self, x, logits, stream=None, events=None, splits=None, mark=None):
@@ -276,8 +298,8 @@ class MoELayer:
             p.rank_views(r)["send"].cpu().numpy()   # host sync for the split sizes
         _mark("route")
         j, n, h = self.group, self.n, self.h
-        send_rows = int(S[j].sum())
-        recv_rows = int(S[:, j].sum())
+        in_split, out_split = baseline_splits(S, j)
+        send_rows, recv_rows = sum(in_split), sum(out_split)
         key = (send_rows, recv_rows)
         if getattr(self, "_bl_key", None) != key:
             dev = x.device
@@ -290,8 +312,6 @@ class MoELayer:
                 cnt=torch.empty(n, dtype=torch.int32, device=dev))
             self._bl_key = key
         b = self._bl_bufs
-        out_split = [int(v) for v in S[:, j]]
-        in_split = [int(v) for v in S[j]]
         N.check(lib.mx_baseline_dispatch_pack(p._plan, r, C.c_void_p(x.data_ptr()),
                                               C.c_void_p(b["send"].data_ptr()),
                                               C.c_void_p(b["cnt"].data_ptr()), sp), "pack")
