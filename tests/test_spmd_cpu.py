@@ -40,11 +40,14 @@ from paper_2601_08800_b200.simcluster import expert_home_node
 T, H, E, K = 24, 10, 12, 3     # h=10 splits unevenly over 4 TP ranks (3,3,2,2)
 
 
-def _inputs(n, seed):
-    """The same seeded global batch on every rank (distinct experts/token)."""
+def _inputs(n, seed, empty_host=False):
+    """The same seeded global batch on every rank (distinct experts/token);
+    ``empty_host``: no token routes to the last node's experts, so it
+    receives nothing and sends nothing back (zero splits both ways)."""
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((n * T, H))
-    ids = np.stack([rng.permutation(E)[:K] for _ in range(n * T)]).astype(np.int64)
+    pool = E if not empty_host else -(-(n - 1) * E // n)   # experts homed on nodes < n-1
+    ids = np.stack([rng.permutation(pool)[:K] for _ in range(n * T)]).astype(np.int64)
     w = rng.random((n * T, K))
     scales = rng.uniform(0.5, 1.5, E)
     biases = rng.standard_normal(E)
@@ -73,24 +76,26 @@ def _a2a(chunks, group=None):
     return np.split(recv.numpy(), np.cumsum(out_sizes.tolist())[:-1])
 
 
-def _worker(rank, world, tp, port, seed):
+def _worker(rank, world, tp, port, seed, empty_host):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        _check_rank(rank, world, tp, seed)
+        _check_rank(rank, world, tp, seed, empty_host)
     finally:
         dist.destroy_process_group()
 
 
-def _check_rank(rank, world, tp, seed):
+def _check_rank(rank, world, tp, seed, empty_host):
     n, m = layout_for(world, tp)
     node, t = divmod(rank, m)
     ep_g, tp_g = tp_ep_groups(n, m, rank)
     assert dist.get_world_size(ep_g) == n and dist.get_world_size(tp_g) == m
     assert dist.get_rank(ep_g) == node and dist.get_rank(tp_g) == t
 
-    x, ids, w, scales, biases = _inputs(n, seed)
+    x, ids, w, scales, biases = _inputs(n, seed, empty_host)
     table = orc.Table(ids, w, n, T, E)
+    if empty_host:
+        assert table.slots(n - 1) == 0 and table.slots(0) > 0
     S, _ = routing_stats(ids, n, E)
     assert np.array_equal(S, table.send_counts())
     assert all(int(expert_home_node(e, n, E)) == int(orc.home(e, n, E)) for e in range(E))
@@ -116,7 +121,7 @@ def _check_rank(rank, world, tp, seed):
     for src in range(world):
         j, ts = divmod(src, m)
         rows = table.rows_from(node, j)
-        recv[np.ix_(rows, np.arange(H)[cols[ts]])] = got[src].reshape(len(rows), -1)
+        recv[np.ix_(rows, np.arange(H)[cols[ts]])] = got[src].reshape(len(rows), cols[ts].stop - cols[ts].start)
     assert np.array_equal(recv, recv_ref)                  # bit-exact rows
 
     part = _partial(recv, table.expert[node], scales, biases, cols[t], m)
@@ -182,9 +187,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,tp", [(2, 1), (2, 2), (4, 2), (4, 4), (8, 2)])
-def test_spmd_exchange_gloo(world, tp):
-    mp.spawn(_worker, args=(world, tp, _free_port(), 1000 + 10 * world + tp),
+@pytest.mark.parametrize("world,tp,empty_host", [(2, 1, False), (2, 2, False), (4, 2, False),
+                                                 (4, 4, False), (8, 2, False), (4, 1, True),
+                                                 (4, 2, True)])
+def test_spmd_exchange_gloo(world, tp, empty_host):
+    mp.spawn(_worker, args=(world, tp, _free_port(), 1000 + 10 * world + tp, empty_host),
              nprocs=world, join=True)
 
 
